@@ -1,0 +1,167 @@
+/*
+ * pmg_b200.h — C-ABI of the B200-native vertex-patch multigrid hot path.
+ *
+ * Drop-in boundary for the reference library `pmg` (/root/reference/proj).
+ * Every entry point below replaces one reference function; the citation is the
+ * reference declaration it stands in for. Plain C types only: opaque handles,
+ * device or host pointers, int64 sizes, a cudaStream_t passed as void*.
+ * No exceptions cross this boundary; every call returns a pmg_status.
+ *
+ * Vectors use the reference layout unchanged (mesh.cpp:42-57): a flat array of
+ * N = m^d values of the level's interior nodes, lexicographic with direction 0
+ * fastest, homogeneous Dirichlet nodes eliminated. T is double (PMG_F64) or
+ * float (PMG_F32), fixed per context like the reference's explicit
+ * instantiations (smoother.cpp:153-158, multigrid.cpp:46-51).
+ *
+ * Device-pointer entry points enqueue on `stream` and return without
+ * synchronising. *_host entry points take host pointers and are synchronous
+ * (H2D, compute, D2H) — the reference's std::span calling convention.
+ */
+#ifndef PMG_B200_H
+#define PMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum
+{
+  PMG_OK = 0,
+  PMG_ERR_INVALID = 1,    /* std::invalid_argument in the reference        */
+  PMG_ERR_RUNTIME = 2,    /* std::runtime_error / std::logic_error          */
+  PMG_ERR_DIVERGENCE = 3, /* pmg::DivergenceError (multigrid.hpp:22-29)     */
+  PMG_ERR_CUDA = 4        /* CUDA launch / allocation failure               */
+} pmg_status;
+
+typedef enum
+{
+  PMG_F64 = 0,
+  PMG_F32 = 1
+} pmg_dtype;
+
+/* SmootherVariant, smoother.hpp:21-27 (same numbering). */
+typedef enum
+{
+  PMG_GLOBAL = 0,
+  PMG_SEPARATE = 1,
+  PMG_FUSED = 2,
+  PMG_BOUNDARY = 3,
+  PMG_NAIVE = 100 /* straightforward global-memory fused kernel (the "≥2×"
+                     comparator of the north star); same result as FUSED */
+} pmg_variant;
+
+typedef struct pmg_level_s *pmg_level; /* ~ LevelContext<T>     (level_context.hpp:17-26) */
+typedef struct pmg_mg_s *pmg_mg;       /* ~ MultigridContext<T> (multigrid.hpp:34-49)     */
+
+/* Last error message of the calling thread (static storage, never NULL). */
+const char *pmg_last_error(void);
+
+/* Library / device facts used by the bench and the tests. */
+int pmg_version(void);
+int pmg_device_info(int device, int *sm_count, int *sm_clock_khz, int *cc_major,
+                    int *cc_minor);
+
+/* ---- level context ------------------------------------------------------
+ * ~ make_level_context<T>(build_hierarchy(dim, degree, level).back())
+ *   (level_context.cpp:9-36, mesh.cpp:12-40). Setup (1D matrices, generalized
+ *   eigenpairs, prolongation matrix) runs on the host in f64, is cast to T
+ *   and uploaded once. */
+int pmg_level_create(int dim, int degree, int level, int dtype, int device, pmg_level *out);
+int pmg_level_destroy(pmg_level h);
+/* m (dofs per dim), N (total dofs), patches (n-1)^d */
+int pmg_level_info(pmg_level h, int64_t *dofs_per_dim, int64_t *total_dofs,
+                   int64_t *patches);
+
+/* ~ smooth<T>(ctx, x, b, variant, threads, ws)   smoother.hpp:45-47
+ *   One colourised multiplicative vertex-patch step, colours in ascending
+ *   parity code; x updated in place. */
+int pmg_smooth(pmg_level h, int variant, void *x, const void *b, void *stream);
+int pmg_smooth_host(pmg_level h, int variant, void *x, const void *b);
+
+/* One colour of the step only (for the multi-GPU slab driver and tests). */
+int pmg_smooth_color(pmg_level h, int variant, int color, void *x, const void *b,
+                     void *stream);
+
+/* ~ apply_laplacian<T>(level, cell_mass, cell_stiffness, x, y, mode, threads)
+ *   operator.hpp:47-50 — y = A_l x. */
+int pmg_apply_laplacian(pmg_level h, const void *x, void *y, void *stream);
+int pmg_apply_laplacian_host(pmg_level h, const void *x, void *y);
+
+/* ~ compute_residual<T>(lev, x, b, r, threads)   multigrid.hpp:90-92 */
+int pmg_compute_residual(pmg_level h, const void *x, const void *b, void *r, void *stream);
+int pmg_compute_residual_host(pmg_level h, const void *x, const void *b, void *r);
+
+/* ~ prolongate<T>(coarse, fine, x_coarse, x_fine)   multigrid.hpp:56-58
+ *   (accumulate != 0 gives x_fine += P x_coarse, the V-cycle's correction) */
+int pmg_prolongate(pmg_level coarse, pmg_level fine, const void *xc, void *xf, int accumulate,
+                   void *stream);
+int pmg_prolongate_host(pmg_level coarse, pmg_level fine, const void *xc, void *xf);
+
+/* ~ restrict_vector<T>(coarse, fine, r_fine, r_coarse)   multigrid.hpp:61-63 */
+int pmg_restrict_vector(pmg_level coarse, pmg_level fine, const void *rf, void *rc,
+                        void *stream);
+int pmg_restrict_vector_host(pmg_level coarse, pmg_level fine, const void *rf, void *rc);
+
+/* ~ vector_norm(v)   multigrid.hpp:89 — deterministic two-pass reduction in
+ *   f64 (also for f32 vectors); synchronises `stream`. */
+int pmg_vector_norm(pmg_level h, const void *v, double *out, void *stream);
+/* Same for an arbitrary device vector of n entries of `dtype` on `device`. */
+int pmg_norm2(const void *v, int64_t n, int dtype, int device, double *out, void *stream);
+
+/* ---- multigrid context --------------------------------------------------
+ * ~ make_multigrid_context<T>(dim, degree, finest_level, variant, kind,
+ *   threads)   multigrid.hpp:51-54 (kind = vertex_patch). */
+int pmg_mg_create(int dim, int degree, int finest_level, int dtype, int variant, int device,
+                  pmg_mg *out);
+int pmg_mg_destroy(pmg_mg h);
+int pmg_mg_num_levels(pmg_mg h);
+pmg_level pmg_mg_level(pmg_mg h, int li); /* borrowed; index 0 = mesh level 1 */
+int pmg_mg_set_smoothing(pmg_mg h, int pre_smooth, int post_smooth);
+int pmg_mg_set_variant(pmg_mg h, int variant);
+
+/* ~ v_cycle<T>(ctx, li, x, b)   multigrid.hpp:68-69. use_graph != 0 replays a
+ *   CUDA graph of the whole cycle (captured on first use for this (li, x, b)). */
+int pmg_v_cycle(pmg_mg h, int li, void *x, const void *b, int use_graph, void *stream);
+int pmg_v_cycle_host(pmg_mg h, int li, void *x, const void *b);
+
+/* ~ full_multigrid(ctx, rhs_per_level, x, tol, max_iterations)
+ *   multigrid.hpp:80-86 (f64 contexts only, like the reference). rhs[li] are
+ *   device pointers, one per level; x (device) receives the solution.
+ *   history (capacity history_cap) receives ||b|| then ||r|| per V-cycle.
+ *   Returns PMG_ERR_DIVERGENCE after max_iterations, like DivergenceError. */
+int pmg_full_multigrid(pmg_mg h, const void *const *rhs_per_level, void *x, double tol,
+                       int max_iterations, int *iterations, double *history, int history_cap,
+                       void *stream);
+
+/* ~ compute_rhs(level, f)   operator.hpp:58-59, for f = 1 (kind 0) and
+ *   f = d pi^2 prod sin(pi x_a) (kind 1); host output in f64. */
+int pmg_compute_rhs_host(int dim, int degree, int level, int kind, double *out);
+/* ~ l2_error(level, x, u)   operator.hpp:62-64 for u = prod sin(pi x_a). */
+int pmg_l2_error_sin_host(int dim, int degree, int level, const double *x, double *out);
+
+/* ---- mixed precision / Krylov (krylov.hpp:30-39) -------------------------
+ * Right-preconditioned GMRES(restart) in f64 on the device with the V-cycle
+ * of `prec` (an f32 context: mixed precision; an f64 context: double) as the
+ * preconditioner; operator = f64 level operator of `op`'s finest level. */
+int pmg_gmres(pmg_mg op, pmg_mg prec, const void *b, void *x, double tol, int restart,
+              int max_iterations, int *iterations, double *history, int history_cap,
+              void *stream);
+
+/* ---- raw kernels (tests / bench) ----------------------------------------- */
+/* Setup data of a level as uploaded (f64 copies), for parity tests:
+ * S (ni*ni row-major), lambda (ni), mass_if, stiff_if (ni*nc), prolongation
+ * ((2k+1)*(k+1)), cell mass/stiffness ((k+1)^2). Any pointer may be NULL. */
+int pmg_level_setup_data(pmg_level h, double *S, double *lambda, double *mass_if,
+                         double *stiff_if, double *prolongation, double *cell_mass,
+                         double *cell_stiffness);
+
+/* Number of kernel launches issued by this library since load (counter). */
+int64_t pmg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMG_B200_H */

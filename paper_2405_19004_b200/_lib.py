@@ -1,0 +1,96 @@
+"""ctypes binding of the C-ABI (include/pmg_b200.h).
+
+The shared library is built in-tree (paper_2405_19004_b200/libpmg_b200.so,
+see __graft_entry__.build()). There is no fallback: if the library is missing
+every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpmg_b200.so")
+
+PMG_OK, PMG_ERR_INVALID, PMG_ERR_RUNTIME, PMG_ERR_DIVERGENCE, PMG_ERR_CUDA = range(5)
+PMG_F64, PMG_F32 = 0, 1
+VARIANTS = {"global": 0, "separate": 1, "fused": 2, "boundary": 3, "naive": 100}
+
+# (name, restype, argtypes) for every symbol declared in include/pmg_b200.h
+_vp, _i, _i64, _d = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+_pi64, _pd, _pi = ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)
+SIGNATURES = [
+    ("pmg_last_error", ctypes.c_char_p, []),
+    ("pmg_version", _i, []),
+    ("pmg_device_info", _i, [_i, _pi, _pi, _pi, _pi]),
+    ("pmg_level_create", _i, [_i, _i, _i, _i, _i, ctypes.POINTER(_vp)]),
+    ("pmg_level_destroy", _i, [_vp]),
+    ("pmg_level_info", _i, [_vp, _pi64, _pi64, _pi64]),
+    ("pmg_smooth", _i, [_vp, _i, _vp, _vp, _vp]),
+    ("pmg_smooth_host", _i, [_vp, _i, _vp, _vp]),
+    ("pmg_smooth_color", _i, [_vp, _i, _i, _vp, _vp, _vp]),
+    ("pmg_apply_laplacian", _i, [_vp, _vp, _vp, _vp]),
+    ("pmg_apply_laplacian_host", _i, [_vp, _vp, _vp]),
+    ("pmg_compute_residual", _i, [_vp, _vp, _vp, _vp, _vp]),
+    ("pmg_compute_residual_host", _i, [_vp, _vp, _vp, _vp]),
+    ("pmg_prolongate", _i, [_vp, _vp, _vp, _vp, _i, _vp]),
+    ("pmg_prolongate_host", _i, [_vp, _vp, _vp, _vp]),
+    ("pmg_restrict_vector", _i, [_vp, _vp, _vp, _vp, _vp]),
+    ("pmg_restrict_vector_host", _i, [_vp, _vp, _vp, _vp]),
+    ("pmg_vector_norm", _i, [_vp, _vp, _pd, _vp]),
+    ("pmg_norm2", _i, [_vp, _i64, _i, _i, _pd, _vp]),
+    ("pmg_mg_create", _i, [_i, _i, _i, _i, _i, _i, ctypes.POINTER(_vp)]),
+    ("pmg_mg_destroy", _i, [_vp]),
+    ("pmg_mg_num_levels", _i, [_vp]),
+    ("pmg_mg_level", _vp, [_vp, _i]),
+    ("pmg_mg_set_smoothing", _i, [_vp, _i, _i]),
+    ("pmg_mg_set_variant", _i, [_vp, _i]),
+    ("pmg_v_cycle", _i, [_vp, _i, _vp, _vp, _i, _vp]),
+    ("pmg_v_cycle_host", _i, [_vp, _i, _vp, _vp]),
+    ("pmg_full_multigrid", _i, [_vp, ctypes.POINTER(_vp), _vp, _d, _i, _pi, _pd, _i, _vp]),
+    ("pmg_compute_rhs_host", _i, [_i, _i, _i, _i, _pd]),
+    ("pmg_l2_error_sin_host", _i, [_i, _i, _i, _pd, _pd]),
+    ("pmg_gmres", _i, [_vp, _vp, _vp, _vp, _d, _i, _i, _pi, _pd, _i, _vp]),
+    ("pmg_level_setup_data", _i, [_vp, _pd, _pd, _pd, _pd, _pd, _pd, _pd]),
+    ("pmg_launch_count", _i64, []),
+]
+
+_lib = None
+
+
+def load():
+    """Load the in-tree C-ABI library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+class DivergenceError(RuntimeError):
+    """pmg::DivergenceError (multigrid.hpp:22-29): carries the residual history."""
+
+    def __init__(self, msg, residual_history=None):
+        super().__init__(msg)
+        self.residual_history = list(residual_history or [])
+
+
+def check(status: int, what: str = "", history=None) -> None:
+    if status == PMG_OK:
+        return
+    msg = load().pmg_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if status == PMG_ERR_INVALID:
+        raise ValueError(text)
+    if status == PMG_ERR_DIVERGENCE:
+        raise DivergenceError(text, history)
+    raise RuntimeError(text)

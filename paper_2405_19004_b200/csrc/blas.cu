@@ -1,0 +1,170 @@
+// Level-vector kernels: deterministic reductions and elementwise updates.
+//
+// vector_norm (/root/reference/proj/src/multigrid.cpp:260-266) and the dot /
+// axpy / cast loops of the Krylov driver (krylov.cpp:13-171). Reductions are
+// two-pass with a fixed grid and a fixed tree, so results are bitwise
+// reproducible run to run (no atomics), accumulated in f64.
+#include "blas.cuh"
+
+namespace pmgb
+{
+
+namespace
+{
+
+constexpr int RED_THREADS = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(RED_THREADS)
+    dot_partial_kernel(const T *__restrict__ a, const T *__restrict__ b, int64_t n,
+                       double *__restrict__ partial)
+{
+  __shared__ double sh[RED_THREADS];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = per * blockIdx.x;
+  const int64_t hi = min(n, lo + per);
+  double s = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += RED_THREADS)
+    s = fma(static_cast<double>(a[i]), static_cast<double>(b[i]), s);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = RED_THREADS / 2; w > 0; w >>= 1)
+  {
+    if (threadIdx.x < w)
+      sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    partial[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+    finish_kernel(const double *__restrict__ partial, int np, double *__restrict__ out, int sqrt_it)
+{
+  __shared__ double sh[RED_THREADS];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += RED_THREADS)
+    s += partial[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = RED_THREADS / 2; w > 0; w >>= 1)
+  {
+    if (threadIdx.x < w)
+      sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    *out = sqrt_it ? sqrt(sh[0]) : sh[0];
+}
+
+template <typename T>
+__global__ void fill_kernel(T *x, int64_t n, T v)
+{
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    x[i] = v;
+}
+
+// y = alpha * x + beta * y
+template <typename T>
+__global__ void axpby_kernel(T alpha, const T *__restrict__ x, T beta, T *__restrict__ y, int64_t n)
+{
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = alpha * x[i] + beta * y[i];
+}
+
+// y = alpha_dev[0] * x + y  (device-side coefficient, for graph-friendly MGS)
+__global__ void axpy_dev_kernel(const double *__restrict__ alpha, double scale,
+                                const double *__restrict__ x, double *__restrict__ y, int64_t n)
+{
+  const double a = scale * alpha[0];
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+
+__global__ void d2f_kernel(const double *__restrict__ x, float *__restrict__ y, int64_t n,
+                           int *__restrict__ nonfinite)
+{
+  int bad = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+  {
+    const float v = static_cast<float>(x[i]);
+    if (!isfinite(v))
+      bad = 1;
+    y[i] = v;
+  }
+  if (bad)
+    *nonfinite = 1;  // benign race: every writer stores 1
+}
+
+__global__ void f2d_kernel(const float *__restrict__ x, double *__restrict__ y, int64_t n)
+{
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = static_cast<double>(x[i]);
+}
+
+unsigned ew_grid(int64_t n, int sm_count)
+{
+  const int64_t b = (n + 255) / 256;
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(b, static_cast<int64_t>(sm_count) * 16)));
+}
+
+}  // namespace
+
+template <typename T>
+void launch_dot(const T *a, const T *b, int64_t n, double *partial, double *out, bool sqrt_it,
+                cudaStream_t s)
+{
+  dot_partial_kernel<T><<<RED_BLOCKS, RED_THREADS, 0, s>>>(a, b, n, partial);
+  check_launch("dot_partial_kernel");
+  finish_kernel<<<1, RED_THREADS, 0, s>>>(partial, RED_BLOCKS, out, sqrt_it ? 1 : 0);
+  check_launch("finish_kernel");
+}
+
+template <typename T>
+void launch_fill(T *x, int64_t n, T v, int sm_count, cudaStream_t s)
+{
+  if (n == 0)
+    return;
+  fill_kernel<T><<<ew_grid(n, sm_count), 256, 0, s>>>(x, n, v);
+  check_launch("fill_kernel");
+}
+
+template <typename T>
+void launch_axpby(T alpha, const T *x, T beta, T *y, int64_t n, int sm_count, cudaStream_t s)
+{
+  axpby_kernel<T><<<ew_grid(n, sm_count), 256, 0, s>>>(alpha, x, beta, y, n);
+  check_launch("axpby_kernel");
+}
+
+void launch_axpy_dev(const double *alpha, double scale, const double *x, double *y, int64_t n,
+                     int sm_count, cudaStream_t s)
+{
+  axpy_dev_kernel<<<ew_grid(n, sm_count), 256, 0, s>>>(alpha, scale, x, y, n);
+  check_launch("axpy_dev_kernel");
+}
+
+void launch_d2f(const double *x, float *y, int64_t n, int *nonfinite, int sm_count, cudaStream_t s)
+{
+  d2f_kernel<<<ew_grid(n, sm_count), 256, 0, s>>>(x, y, n, nonfinite);
+  check_launch("d2f_kernel");
+}
+
+void launch_f2d(const float *x, double *y, int64_t n, int sm_count, cudaStream_t s)
+{
+  f2d_kernel<<<ew_grid(n, sm_count), 256, 0, s>>>(x, y, n);
+  check_launch("f2d_kernel");
+}
+
+template void launch_dot<double>(const double *, const double *, int64_t, double *, double *, bool, cudaStream_t);
+template void launch_dot<float>(const float *, const float *, int64_t, double *, double *, bool, cudaStream_t);
+template void launch_fill<double>(double *, int64_t, double, int, cudaStream_t);
+template void launch_fill<float>(float *, int64_t, float, int, cudaStream_t);
+template void launch_axpby<double>(double, const double *, double, double *, int64_t, int, cudaStream_t);
+template void launch_axpby<float>(float, const float *, float, float *, int64_t, int, cudaStream_t);
+
+}  // namespace pmgb

@@ -1,0 +1,22 @@
+#pragma once
+#include "common.cuh"
+
+namespace pmgb
+{
+
+constexpr int RED_BLOCKS = 1024;  // fixed grid of the two-pass reductions
+
+// out[0] = sum a_i b_i (sqrt_it: sqrt of it); partial >= RED_BLOCKS doubles
+template <typename T>
+void launch_dot(const T *a, const T *b, int64_t n, double *partial, double *out, bool sqrt_it,
+                cudaStream_t s);
+template <typename T>
+void launch_fill(T *x, int64_t n, T v, int sm_count, cudaStream_t s);
+template <typename T>
+void launch_axpby(T alpha, const T *x, T beta, T *y, int64_t n, int sm_count, cudaStream_t s);
+void launch_axpy_dev(const double *alpha, double scale, const double *x, double *y, int64_t n,
+                     int sm_count, cudaStream_t s);
+void launch_d2f(const double *x, float *y, int64_t n, int *nonfinite, int sm_count, cudaStream_t s);
+void launch_f2d(const float *x, double *y, int64_t n, int sm_count, cudaStream_t s);
+
+}  // namespace pmgb

@@ -1,0 +1,1030 @@
+// C-ABI implementation (include/pmg_b200.h): level / multigrid contexts,
+// the colour loop of the smoother, the V-cycle, FMG and GMRES drivers.
+//
+// Host-side control flow mirrors the reference call graph
+// (smoother.cpp:41-151, multigrid.cpp:286-400, krylov.cpp:24-171); every
+// arithmetic step runs in a CUDA kernel on the context's device. There is no
+// CPU fallback: a missing device or a failed launch is an error.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/pmg_b200.h"
+#include "blas.cuh"
+#include "dispatch.hpp"
+#include "naive.cuh"
+#include "setup.hpp"
+#include "capi_internal.hpp"
+
+namespace pmgb
+{
+
+namespace
+{
+std::atomic<int64_t> g_launches{0};
+thread_local std::string g_last_error;
+}  // namespace
+
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void check_launch(const char *what)
+{
+  check_cuda(cudaGetLastError(), what);
+  note_launch(1);
+}
+
+Tables &tables()
+{
+  static Tables *t = [] {
+    auto *tb = new Tables();
+    register_k1(*tb);
+    register_k2(*tb);
+    register_k3(*tb);
+    register_k4(*tb);
+    register_k5(*tb);
+    register_k6(*tb);
+    register_k7(*tb);
+    return tb;
+  }();
+  return *t;
+}
+
+struct InvalidArg : std::invalid_argument
+{
+  using std::invalid_argument::invalid_argument;
+};
+using Divergence = DivergenceErr;
+using DeviceGuard = DevScope;
+
+}  // namespace pmgb
+
+using namespace pmgb;
+
+struct pmg_level_s
+{
+  LevelSetup S;
+  int dtype = PMG_F64;
+  int device = 0;
+  int sm_count = 148;
+  size_t tsize = 8;
+  std::vector<unsigned char> patch_mats, band_mats, prol_mats;  // param blobs in T
+  DevBuf inv;             // inverse eigenvalue sums (T)
+  DevBuf resid;           // global residual (global / separate variants)
+  DevBuf naive_mats;      // Mif | Aif | S (T) for the straightforward kernel
+  DevBuf naive_scratch;
+  DevBuf tA, tB;          // transfer scratch (used when this level is the fine one)
+  DevBuf red;             // reduction partials + result (double)
+  DevBuf io[3];           // staging for the *_host entry points
+  cudaStream_t io_stream = nullptr;
+};
+
+struct CachedGraph
+{
+  cudaGraphExec_t exec = nullptr;
+  int li = -1;
+  void *x = nullptr;
+  const void *b = nullptr;
+  int variant = -1, pre = -1, post = -1;
+};
+
+struct pmg_mg_s
+{
+  std::vector<pmg_level> levels;
+  int dtype = PMG_F64;
+  int device = 0;
+  int variant = PMG_FUSED;
+  int pre = 1, post = 1;
+  std::vector<DevBuf *> r_ws, bc_ws, xc_ws;  // per level li (sizes: N_li, N_{li-1}, N_{li-1})
+  CachedGraph graph;
+  cudaStream_t cap_stream = nullptr;
+  DevBuf fmg_x[32];
+  GmresWork gmres;
+  ~pmg_mg_s()
+  {
+    if (graph.exec)
+      cudaGraphExecDestroy(graph.exec);
+    if (cap_stream)
+      cudaStreamDestroy(cap_stream);
+    for (auto *b : r_ws)
+      delete b;
+    for (auto *b : bc_ws)
+      delete b;
+    for (auto *b : xc_ws)
+      delete b;
+    for (auto *l : levels)
+      delete l;
+  }
+};
+
+namespace
+{
+
+template <typename F>
+int guard(F &&f)
+{
+  return capi_guard(std::forward<F>(f));
+}
+
+inline cudaStream_t as_stream(void *s) { return static_cast<cudaStream_t>(s); }
+
+template <typename T>
+const KernelTable<T> &ktab(const pmg_level_s *l);
+template <>
+const KernelTable<double> &ktab<double>(const pmg_level_s *l)
+{
+  return tables().f64[l->S.dim - 2][l->S.k];
+}
+template <>
+const KernelTable<float> &ktab<float>(const pmg_level_s *l)
+{
+  return tables().f32[l->S.dim - 2][l->S.k];
+}
+
+template <typename T>
+std::vector<unsigned char> blob(std::initializer_list<const Dense *> mats)
+{
+  std::vector<T> v;
+  for (const Dense *d : mats)
+    for (double a : d->a)
+      v.push_back(static_cast<T>(a));
+  std::vector<unsigned char> out(v.size() * sizeof(T));
+  std::memcpy(out.data(), v.data(), out.size());
+  return out;
+}
+
+template <typename T>
+std::vector<unsigned char> blob_vec(const std::vector<double> &a, const std::vector<double> &b)
+{
+  std::vector<T> v;
+  for (double x : a)
+    v.push_back(static_cast<T>(x));
+  for (double x : b)
+    v.push_back(static_cast<T>(x));
+  std::vector<unsigned char> out(v.size() * sizeof(T));
+  std::memcpy(out.data(), v.data(), out.size());
+  return out;
+}
+
+template <typename T>
+void upload(DevBuf &buf, const std::vector<double> &host)
+{
+  std::vector<T> v(host.begin(), host.end());
+  buf.ensure(v.size() * sizeof(T));
+  check_cuda(cudaMemcpy(buf.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice),
+             "upload");
+}
+
+template <typename T>
+void level_init(pmg_level_s *l)
+{
+  const auto &S = l->S;
+  l->patch_mats = blob<T>({&S.mass_if, &S.stiff_if, &S.S});
+  l->band_mats = blob_vec<T>(S.band_mass, S.band_stiff);
+  l->prol_mats = blob<T>({&S.prolongation});
+  upload<T>(l->inv, S.inv_sums);
+  std::vector<double> nm;
+  nm.insert(nm.end(), S.mass_if.a.begin(), S.mass_if.a.end());
+  nm.insert(nm.end(), S.stiff_if.a.begin(), S.stiff_if.a.end());
+  nm.insert(nm.end(), S.S.a.begin(), S.S.a.end());
+  upload<T>(l->naive_mats, nm);
+  l->red.ensure((RED_BLOCKS + 8) * sizeof(double));
+}
+
+// patches of colour `color` (patches.cpp:11-46): v_a in {1,3,..} if bit set else {2,4,..}
+template <typename T>
+ColorArgs<T> color_args(const pmg_level_s *l, int color, T *x, const T *b)
+{
+  ColorArgs<T> a{};
+  a.x = x;
+  a.b = b;
+  a.r = l->resid.as<T>();
+  a.inv = l->inv.as<T>();
+  a.m = l->S.m;
+  const int n = l->S.n;
+  a.total = 1;
+  for (int q = 0; q < 3; ++q)
+  {
+    if (q < l->S.dim)
+    {
+      const int bit = (color >> q) & 1;
+      a.np[q] = bit ? n / 2 : n / 2 - 1;
+      a.vb[q] = bit ? 1 : 2;
+    }
+    else
+    {
+      a.np[q] = 1;
+      a.vb[q] = 1;
+    }
+    a.total *= a.np[q];
+  }
+  return a;
+}
+
+template <typename T>
+void smooth_color_impl(pmg_level_s *l, int variant, int color, T *x, const T *b, cudaStream_t s)
+{
+  const auto &kt = ktab<T>(l);
+  ColorArgs<T> a = color_args<T>(l, color, x, b);
+  if (a.total == 0)
+    return;  // smoother.cpp:57-59: empty colours are skipped
+  switch (variant)
+  {
+    case PMG_FUSED:
+      kt.smooth(l->patch_mats.data(), a, MODE_FUSED, s);
+      break;
+    case PMG_BOUNDARY:
+      kt.smooth(l->patch_mats.data(), a, MODE_BOUNDARY, s);
+      break;
+    case PMG_SEPARATE:
+      l->resid.ensure(static_cast<size_t>(l->S.N) * sizeof(T));
+      a.r = l->resid.as<T>();
+      kt.smooth(l->patch_mats.data(), a, MODE_RESIDUAL, s);
+      kt.smooth(l->patch_mats.data(), a, MODE_SOLVE, s);
+      break;
+    case PMG_GLOBAL:
+      l->resid.ensure(static_cast<size_t>(l->S.N) * sizeof(T));
+      a.r = l->resid.as<T>();
+      kt.level_op(l->band_mats.data(), x, b, a.r, l->S.m, l->sm_count, s);
+      kt.smooth(l->patch_mats.data(), a, MODE_SOLVE, s);
+      break;
+    case PMG_NAIVE:
+    {
+      const int grid = l->sm_count * 16;
+      const int64_t per = naive_scratch_per_block<T>(l->S.dim, l->S.k);
+      l->naive_scratch.ensure(static_cast<size_t>(per) * grid * sizeof(T));
+      NaiveArgs<T> na{};
+      na.c = a;
+      const int ni = 2 * l->S.k - 1, nc = 2 * l->S.k + 1;
+      na.Mif = l->naive_mats.as<T>();
+      na.Aif = na.Mif + ni * nc;
+      na.S = na.Aif + ni * nc;
+      na.dim = l->S.dim;
+      na.k = l->S.k;
+      na.scratch = l->naive_scratch.as<T>();
+      na.scratch_stride = per;
+      launch_naive_smooth<T>(na, grid, s);
+      break;
+    }
+    default:
+      throw InvalidArg("smooth: unknown variant " + std::to_string(variant));
+  }
+}
+
+template <typename T>
+void smooth_impl(pmg_level_s *l, int variant, T *x, const T *b, cudaStream_t s)
+{
+  for (int color = 0; color < (1 << l->S.dim); ++color)
+    smooth_color_impl<T>(l, variant, color, x, b, s);
+}
+
+void check_pair(const pmg_level_s *c, const pmg_level_s *f, const char *what)
+{
+  if (!c || !f)
+    throw InvalidArg(std::string(what) + ": null level");
+  if (f->S.level != c->S.level + 1 || f->S.k != c->S.k || f->S.dim != c->S.dim ||
+      f->dtype != c->dtype || f->device != c->device)
+    throw InvalidArg(std::string(what) + ": levels are not consecutive");
+}
+
+template <typename T>
+void transfer_scratch(pmg_level_s *fine)
+{
+  const int64_t mf = fine->S.m, mc = (mf - 1) / 2;
+  const int64_t need = fine->S.dim == 3 ? mf * mf * mc : mf * mc;
+  fine->tA.ensure(static_cast<size_t>(need) * sizeof(T));
+  fine->tB.ensure(static_cast<size_t>(need) * sizeof(T));
+}
+
+template <typename T>
+void prolongate_impl(pmg_level_s *c, pmg_level_s *f, const T *xc, T *xf, bool acc, cudaStream_t s)
+{
+  transfer_scratch<T>(f);
+  ktab<T>(f).prolongate(f->prol_mats.data(), xc, xf, acc, c->S.m, f->tA.as<T>(), f->tB.as<T>(),
+                        f->sm_count, s);
+}
+
+template <typename T>
+void restrict_impl(pmg_level_s *c, pmg_level_s *f, const T *rf, T *rc, cudaStream_t s)
+{
+  transfer_scratch<T>(f);
+  ktab<T>(f).restrict_(f->prol_mats.data(), rf, rc, c->S.m, f->tA.as<T>(), f->tB.as<T>(),
+                       f->sm_count, s);
+}
+
+template <typename T>
+double norm_impl(pmg_level_s *l, const T *v, int64_t n, cudaStream_t s)
+{
+  double *red = l->red.as<double>();
+  launch_dot<T>(v, v, n, red, red + RED_BLOCKS, true, s);
+  double out = 0;
+  check_cuda(cudaMemcpyAsync(&out, red + RED_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, s),
+             "norm D2H");
+  check_cuda(cudaStreamSynchronize(s), "norm sync");
+  return out;
+}
+
+template <typename T>
+void vcycle_impl(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s)
+{
+  pmg_level_s *lev = mg->levels[li];
+  if (li == 0)
+  {
+    // coarse_solve (multigrid.cpp:304-309): x = 0, one fused step is exact
+    launch_fill<T>(x, lev->S.N, T(0), lev->sm_count, s);
+    smooth_impl<T>(lev, PMG_FUSED, x, b, s);
+    return;
+  }
+  pmg_level_s *crs = mg->levels[li - 1];
+  for (int i = 0; i < mg->pre; ++i)
+    smooth_impl<T>(lev, mg->variant, x, b, s);
+  T *r = mg->r_ws[li]->as<T>();
+  T *bc = mg->bc_ws[li]->as<T>();
+  T *xc = mg->xc_ws[li]->as<T>();
+  ktab<T>(lev).level_op(lev->band_mats.data(), x, b, r, lev->S.m, lev->sm_count, s);
+  restrict_impl<T>(crs, lev, r, bc, s);
+  if (li - 1 > 0)
+    launch_fill<T>(xc, crs->S.N, T(0), crs->sm_count, s);  // the coarse solve zeroes x itself
+  vcycle_impl<T>(mg, li - 1, xc, bc, s);
+  prolongate_impl<T>(crs, lev, xc, x, true, s);
+  for (int i = 0; i < mg->post; ++i)
+    smooth_impl<T>(lev, mg->variant, x, b, s);
+}
+
+template <typename T>
+void vcycle_entry(pmg_mg_s *mg, int li, T *x, const T *b, bool use_graph, cudaStream_t s)
+{
+  if (!use_graph)
+  {
+    vcycle_impl<T>(mg, li, x, b, s);
+    return;
+  }
+  CachedGraph &g = mg->graph;
+  if (!(g.exec && g.li == li && g.x == x && g.b == b && g.variant == mg->variant &&
+        g.pre == mg->pre && g.post == mg->post))
+  {
+    if (g.exec)
+    {
+      cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+    }
+    if (!mg->cap_stream)
+      check_cuda(cudaStreamCreateWithFlags(&mg->cap_stream, cudaStreamNonBlocking), "stream");
+    // one eager pass first so lazy allocations / function attributes are set
+    // outside the capture; order it after the caller's stream
+    check_cuda(cudaStreamSynchronize(s), "graph pre-sync");
+    cudaGraph_t graph = nullptr;
+    check_cuda(cudaStreamBeginCapture(mg->cap_stream, cudaStreamCaptureModeRelaxed), "capture begin");
+    try
+    {
+      vcycle_impl<T>(mg, li, x, b, mg->cap_stream);
+    }
+    catch (...)
+    {
+      cudaStreamEndCapture(mg->cap_stream, &graph);
+      if (graph)
+        cudaGraphDestroy(graph);
+      throw;
+    }
+    check_cuda(cudaStreamEndCapture(mg->cap_stream, &graph), "capture end");
+    check_cuda(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
+    cudaGraphDestroy(graph);
+    g.li = li;
+    g.x = x;
+    g.b = b;
+    g.variant = mg->variant;
+    g.pre = mg->pre;
+    g.post = mg->post;
+  }
+  check_cuda(cudaGraphLaunch(g.exec, s), "graph launch");
+}
+
+pmg_level_s *make_level(int dim, int k, int level, int dtype, int device)
+{
+  if (dtype != PMG_F64 && dtype != PMG_F32)
+    throw InvalidArg("dtype must be PMG_F64 or PMG_F32");
+  int ndev = 0;
+  check_cuda(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev)
+    throw InvalidArg("no such CUDA device " + std::to_string(device));
+  auto l = std::make_unique<pmg_level_s>();
+  l->S = make_level_setup(dim, k, level);
+  l->dtype = dtype;
+  l->device = device;
+  l->tsize = dtype == PMG_F64 ? 8 : 4;
+  DeviceGuard dg(device);
+  check_cuda(cudaDeviceGetAttribute(&l->sm_count, cudaDevAttrMultiProcessorCount, device), "attr");
+  if (dtype == PMG_F64)
+    level_init<double>(l.get());
+  else
+    level_init<float>(l.get());
+  return l.release();
+}
+
+void require_level(pmg_level h)
+{
+  if (!h)
+    throw InvalidArg("null level handle");
+}
+
+struct HostIO
+{
+  pmg_level_s *l;
+  explicit HostIO(pmg_level_s *lv) : l(lv)
+  {
+    if (!l->io_stream)
+      check_cuda(cudaStreamCreateWithFlags(&l->io_stream, cudaStreamNonBlocking), "stream");
+  }
+  void *dev(int i, size_t bytes)
+  {
+    l->io[i].ensure(bytes);
+    return l->io[i].p;
+  }
+  void h2d(void *d, const void *h, size_t b)
+  {
+    check_cuda(cudaMemcpyAsync(d, h, b, cudaMemcpyHostToDevice, l->io_stream), "H2D");
+  }
+  void d2h(void *h, const void *d, size_t b)
+  {
+    check_cuda(cudaMemcpyAsync(h, d, b, cudaMemcpyDeviceToHost, l->io_stream), "D2H");
+  }
+  void sync() { check_cuda(cudaStreamSynchronize(l->io_stream), "sync"); }
+};
+
+#define PMG_DISPATCH_T(lvl, CALL)  \
+  do                               \
+  {                                \
+    if ((lvl)->dtype == PMG_F64)   \
+    {                              \
+      using T = double;            \
+      CALL;                        \
+    }                              \
+    else                           \
+    {                              \
+      using T = float;             \
+      CALL;                        \
+    }                              \
+  } while (0)
+
+}  // namespace
+
+namespace pmgb
+{
+
+int capi_status_from_current_exception()
+{
+  try
+  {
+    throw;
+  }
+  catch (const std::invalid_argument &e)
+  {
+    g_last_error = e.what();
+    return PMG_ERR_INVALID;
+  }
+  catch (const DivergenceErr &e)
+  {
+    g_last_error = e.what();
+    return PMG_ERR_DIVERGENCE;
+  }
+  catch (const CudaError &e)
+  {
+    g_last_error = e.what();
+    return PMG_ERR_CUDA;
+  }
+  catch (const std::exception &e)
+  {
+    g_last_error = e.what();
+    return PMG_ERR_RUNTIME;
+  }
+  catch (...)
+  {
+    g_last_error = "unknown exception";
+    return PMG_ERR_RUNTIME;
+  }
+}
+
+void GmresWork::ensure(int64_t n, int restart, bool mixed)
+{
+  bV.ensure(static_cast<size_t>(n) * (restart + 1) * sizeof(double));
+  bZ.ensure(static_cast<size_t>(n) * restart * sizeof(double));
+  bw.ensure(static_cast<size_t>(n) * sizeof(double));
+  br.ensure(static_cast<size_t>(n) * sizeof(double));
+  bred.ensure((RED_BLOCKS + 8) * sizeof(double));
+  bflag.ensure(sizeof(int));
+  if (mixed)
+  {
+    brf.ensure(static_cast<size_t>(n) * sizeof(float));
+    bzf.ensure(static_cast<size_t>(n) * sizeof(float));
+  }
+  V = bV.as<double>();
+  Z = bZ.as<double>();
+  w = bw.as<double>();
+  r = br.as<double>();
+  red = bred.as<double>();
+  rf = brf.as<float>();
+  zf = bzf.as<float>();
+  flag = bflag.as<int>();
+}
+
+int mg_dtype(pmg_mg h) { return h->dtype; }
+int mg_device(pmg_mg h) { return h->device; }
+int mg_levels(pmg_mg h) { return static_cast<int>(h->levels.size()); }
+pmg_level mg_level_ptr(pmg_mg h, int li) { return h->levels[li]; }
+int64_t level_total(pmg_level l) { return l->S.N; }
+int level_sm_count(pmg_level l) { return l->sm_count; }
+GmresWork &mg_gmres_work(pmg_mg h) { return h->gmres; }
+
+void mg_apply_finest_op(pmg_mg h, const double *x, double *y, cudaStream_t s)
+{
+  pmg_level_s *l = h->levels.back();
+  ktab<double>(l).level_op(l->band_mats.data(), x, nullptr, y, l->S.m, l->sm_count, s);
+}
+
+void mg_residual_finest(pmg_mg h, const double *x, const double *b, double *r, cudaStream_t s)
+{
+  pmg_level_s *l = h->levels.back();
+  ktab<double>(l).level_op(l->band_mats.data(), x, b, r, l->S.m, l->sm_count, s);
+}
+
+void mg_vcycle_f32(pmg_mg h, int li, float *x, const float *b, cudaStream_t s)
+{
+  vcycle_impl<float>(h, li, x, b, s);
+}
+
+void mg_vcycle_f64(pmg_mg h, int li, double *x, const double *b, cudaStream_t s)
+{
+  vcycle_impl<double>(h, li, x, b, s);
+}
+
+}  // namespace pmgb
+
+extern "C" {
+
+const char *pmg_last_error(void) { return g_last_error.c_str(); }
+
+int pmg_version(void) { return 1; }
+
+int64_t pmg_launch_count(void) { return g_launches.load(); }
+
+int pmg_device_info(int device, int *sm_count, int *sm_clock_khz, int *cc_major, int *cc_minor)
+{
+  return guard([&] {
+    check_cuda(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, device), "attr");
+    check_cuda(cudaDeviceGetAttribute(sm_clock_khz, cudaDevAttrClockRate, device), "attr");
+    check_cuda(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, device), "attr");
+    check_cuda(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, device), "attr");
+  });
+}
+
+int pmg_level_create(int dim, int degree, int level, int dtype, int device, pmg_level *out)
+{
+  return guard([&] {
+    if (!out)
+      throw InvalidArg("null output handle");
+    *out = make_level(dim, degree, level, dtype, device);
+  });
+}
+
+int pmg_level_destroy(pmg_level h)
+{
+  return guard([&] {
+    if (h)
+    {
+      DeviceGuard dg(h->device);
+      if (h->io_stream)
+        cudaStreamDestroy(h->io_stream);
+      delete h;
+    }
+  });
+}
+
+int pmg_level_info(pmg_level h, int64_t *m, int64_t *N, int64_t *patches)
+{
+  return guard([&] {
+    require_level(h);
+    if (m)
+      *m = h->S.m;
+    if (N)
+      *N = h->S.N;
+    if (patches)
+    {
+      int64_t p = 1;
+      for (int a = 0; a < h->S.dim; ++a)
+        p *= (h->S.n - 1);
+      *patches = p;
+    }
+  });
+}
+
+int pmg_level_setup_data(pmg_level h, double *S, double *lambda, double *mass_if, double *stiff_if,
+                         double *prolongation, double *cell_mass, double *cell_stiffness)
+{
+  return guard([&] {
+    require_level(h);
+    auto cp = [](double *dst, const std::vector<double> &v) {
+      if (dst)
+        std::memcpy(dst, v.data(), v.size() * sizeof(double));
+    };
+    cp(S, h->S.S.a);
+    cp(lambda, h->S.lambda);
+    cp(mass_if, h->S.mass_if.a);
+    cp(stiff_if, h->S.stiff_if.a);
+    cp(prolongation, h->S.prolongation.a);
+    cp(cell_mass, h->S.cell_mass.a);
+    cp(cell_stiffness, h->S.cell_stiff.a);
+  });
+}
+
+int pmg_smooth(pmg_level h, int variant, void *x, const void *b, void *stream)
+{
+  return guard([&] {
+    require_level(h);
+    DeviceGuard dg(h->device);
+    PMG_DISPATCH_T(h, smooth_impl<T>(h, variant, static_cast<T *>(x), static_cast<const T *>(b),
+                                     as_stream(stream)));
+  });
+}
+
+int pmg_smooth_color(pmg_level h, int variant, int color, void *x, const void *b, void *stream)
+{
+  return guard([&] {
+    require_level(h);
+    if (color < 0 || color >= (1 << h->S.dim))
+      throw InvalidArg("colour out of range");
+    DeviceGuard dg(h->device);
+    PMG_DISPATCH_T(h, smooth_color_impl<T>(h, variant, color, static_cast<T *>(x),
+                                           static_cast<const T *>(b), as_stream(stream)));
+  });
+}
+
+int pmg_smooth_host(pmg_level h, int variant, void *x, const void *b)
+{
+  return guard([&] {
+    require_level(h);
+    DeviceGuard dg(h->device);
+    HostIO io(h);
+    const size_t bytes = static_cast<size_t>(h->S.N) * h->tsize;
+    void *dx = io.dev(0, bytes), *db = io.dev(1, bytes);
+    io.h2d(dx, x, bytes);
+    io.h2d(db, b, bytes);
+    PMG_DISPATCH_T(h, smooth_impl<T>(h, variant, static_cast<T *>(dx), static_cast<const T *>(db),
+                                     h->io_stream));
+    io.d2h(x, dx, bytes);
+    io.sync();
+  });
+}
+
+int pmg_apply_laplacian(pmg_level h, const void *x, void *y, void *stream)
+{
+  return guard([&] {
+    require_level(h);
+    DeviceGuard dg(h->device);
+    PMG_DISPATCH_T(h, ktab<T>(h).level_op(h->band_mats.data(), static_cast<const T *>(x), nullptr,
+                                          static_cast<T *>(y), h->S.m, h->sm_count,
+                                          as_stream(stream)));
+  });
+}
+
+int pmg_compute_residual(pmg_level h, const void *x, const void *b, void *r, void *stream)
+{
+  return guard([&] {
+    require_level(h);
+    if (!b)
+      throw InvalidArg("compute_residual: null b");
+    DeviceGuard dg(h->device);
+    PMG_DISPATCH_T(h, ktab<T>(h).level_op(h->band_mats.data(), static_cast<const T *>(x),
+                                          static_cast<const T *>(b), static_cast<T *>(r), h->S.m,
+                                          h->sm_count, as_stream(stream)));
+  });
+}
+
+int pmg_apply_laplacian_host(pmg_level h, const void *x, void *y)
+{
+  return guard([&] {
+    require_level(h);
+    DeviceGuard dg(h->device);
+    HostIO io(h);
+    const size_t bytes = static_cast<size_t>(h->S.N) * h->tsize;
+    void *dx = io.dev(0, bytes), *dy = io.dev(1, bytes);
+    io.h2d(dx, x, bytes);
+    PMG_DISPATCH_T(h, ktab<T>(h).level_op(h->band_mats.data(), static_cast<const T *>(dx), nullptr,
+                                          static_cast<T *>(dy), h->S.m, h->sm_count, h->io_stream));
+    io.d2h(y, dy, bytes);
+    io.sync();
+  });
+}
+
+int pmg_compute_residual_host(pmg_level h, const void *x, const void *b, void *r)
+{
+  return guard([&] {
+    require_level(h);
+    DeviceGuard dg(h->device);
+    HostIO io(h);
+    const size_t bytes = static_cast<size_t>(h->S.N) * h->tsize;
+    void *dx = io.dev(0, bytes), *db = io.dev(1, bytes), *dr = io.dev(2, bytes);
+    io.h2d(dx, x, bytes);
+    io.h2d(db, b, bytes);
+    PMG_DISPATCH_T(h, ktab<T>(h).level_op(h->band_mats.data(), static_cast<const T *>(dx),
+                                          static_cast<const T *>(db), static_cast<T *>(dr), h->S.m,
+                                          h->sm_count, h->io_stream));
+    io.d2h(r, dr, bytes);
+    io.sync();
+  });
+}
+
+int pmg_prolongate(pmg_level c, pmg_level f, const void *xc, void *xf, int accumulate, void *stream)
+{
+  return guard([&] {
+    check_pair(c, f, "prolongate");
+    DeviceGuard dg(f->device);
+    PMG_DISPATCH_T(f, prolongate_impl<T>(c, f, static_cast<const T *>(xc), static_cast<T *>(xf),
+                                         accumulate != 0, as_stream(stream)));
+  });
+}
+
+int pmg_prolongate_host(pmg_level c, pmg_level f, const void *xc, void *xf)
+{
+  return guard([&] {
+    check_pair(c, f, "prolongate");
+    DeviceGuard dg(f->device);
+    HostIO io(f);
+    const size_t bc = static_cast<size_t>(c->S.N) * f->tsize, bf = static_cast<size_t>(f->S.N) * f->tsize;
+    void *dxc = io.dev(0, bc), *dxf = io.dev(1, bf);
+    io.h2d(dxc, xc, bc);
+    PMG_DISPATCH_T(f, prolongate_impl<T>(c, f, static_cast<const T *>(dxc), static_cast<T *>(dxf),
+                                         false, f->io_stream));
+    io.d2h(xf, dxf, bf);
+    io.sync();
+  });
+}
+
+int pmg_restrict_vector(pmg_level c, pmg_level f, const void *rf, void *rc, void *stream)
+{
+  return guard([&] {
+    check_pair(c, f, "restrict_vector");
+    DeviceGuard dg(f->device);
+    PMG_DISPATCH_T(f, restrict_impl<T>(c, f, static_cast<const T *>(rf), static_cast<T *>(rc),
+                                       as_stream(stream)));
+  });
+}
+
+int pmg_restrict_vector_host(pmg_level c, pmg_level f, const void *rf, void *rc)
+{
+  return guard([&] {
+    check_pair(c, f, "restrict_vector");
+    DeviceGuard dg(f->device);
+    HostIO io(f);
+    const size_t bc = static_cast<size_t>(c->S.N) * f->tsize, bf = static_cast<size_t>(f->S.N) * f->tsize;
+    void *drf = io.dev(0, bf), *drc = io.dev(1, bc);
+    io.h2d(drf, rf, bf);
+    PMG_DISPATCH_T(f, restrict_impl<T>(c, f, static_cast<const T *>(drf), static_cast<T *>(drc),
+                                       f->io_stream));
+    io.d2h(rc, drc, bc);
+    io.sync();
+  });
+}
+
+int pmg_vector_norm(pmg_level h, const void *v, double *out, void *stream)
+{
+  return guard([&] {
+    require_level(h);
+    if (!out)
+      throw InvalidArg("null output");
+    DeviceGuard dg(h->device);
+    PMG_DISPATCH_T(h, *out = norm_impl<T>(h, static_cast<const T *>(v), h->S.N, as_stream(stream)));
+  });
+}
+
+int pmg_norm2(const void *v, int64_t n, int dtype, int device, double *out, void *stream)
+{
+  return guard([&] {
+    if (!out || (n > 0 && !v))
+      throw InvalidArg("pmg_norm2: null pointer");
+    if (dtype != PMG_F64 && dtype != PMG_F32)
+      throw InvalidArg("pmg_norm2: bad dtype");
+    DeviceGuard dg(device);
+    static thread_local DevBuf red[32];
+    DevBuf &rb = red[device & 31];
+    rb.ensure((RED_BLOCKS + 8) * sizeof(double));
+    cudaStream_t s = as_stream(stream);
+    double *r = rb.as<double>();
+    if (dtype == PMG_F64)
+      launch_dot<double>(static_cast<const double *>(v), static_cast<const double *>(v), n, r,
+                         r + RED_BLOCKS, true, s);
+    else
+      launch_dot<float>(static_cast<const float *>(v), static_cast<const float *>(v), n, r,
+                        r + RED_BLOCKS, true, s);
+    check_cuda(cudaMemcpyAsync(out, r + RED_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    check_cuda(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int pmg_mg_create(int dim, int degree, int finest_level, int dtype, int variant, int device,
+                  pmg_mg *out)
+{
+  return guard([&] {
+    if (!out)
+      throw InvalidArg("null output handle");
+    if (finest_level < 1)
+      throw InvalidArg("finest_level must be >= 1");
+    if (variant != PMG_GLOBAL && variant != PMG_SEPARATE && variant != PMG_FUSED &&
+        variant != PMG_BOUNDARY && variant != PMG_NAIVE)
+      throw InvalidArg("unknown smoother variant");
+    auto mg = std::make_unique<pmg_mg_s>();
+    mg->dtype = dtype;
+    mg->device = device;
+    mg->variant = variant;
+    for (int l = 1; l <= finest_level; ++l)
+      mg->levels.push_back(make_level(dim, degree, l, dtype, device));
+    DeviceGuard dg(device);
+    const size_t ts = dtype == PMG_F64 ? 8 : 4;
+    for (int li = 0; li < finest_level; ++li)
+    {
+      auto *r = new DevBuf();
+      auto *bc = new DevBuf();
+      auto *xc = new DevBuf();
+      mg->r_ws.push_back(r);
+      mg->bc_ws.push_back(bc);
+      mg->xc_ws.push_back(xc);
+      if (li > 0)
+      {
+        r->ensure(static_cast<size_t>(mg->levels[li]->S.N) * ts);
+        bc->ensure(static_cast<size_t>(mg->levels[li - 1]->S.N) * ts);
+        xc->ensure(static_cast<size_t>(mg->levels[li - 1]->S.N) * ts);
+        if (dtype == PMG_F64)
+          transfer_scratch<double>(mg->levels[li]);
+        else
+          transfer_scratch<float>(mg->levels[li]);
+      }
+    }
+    *out = mg.release();
+  });
+}
+
+int pmg_mg_destroy(pmg_mg h)
+{
+  return guard([&] {
+    if (h)
+    {
+      DeviceGuard dg(h->device);
+      for (auto *l : h->levels)
+        if (l->io_stream)
+        {
+          cudaStreamDestroy(l->io_stream);
+          l->io_stream = nullptr;
+        }
+      delete h;
+    }
+  });
+}
+
+int pmg_mg_num_levels(pmg_mg h) { return h ? static_cast<int>(h->levels.size()) : 0; }
+
+pmg_level pmg_mg_level(pmg_mg h, int li)
+{
+  if (!h || li < 0 || li >= static_cast<int>(h->levels.size()))
+    return nullptr;
+  return h->levels[li];
+}
+
+int pmg_mg_set_smoothing(pmg_mg h, int pre, int post)
+{
+  return guard([&] {
+    if (!h || pre < 0 || post < 0)
+      throw InvalidArg("invalid smoothing counts");
+    h->pre = pre;
+    h->post = post;
+  });
+}
+
+int pmg_mg_set_variant(pmg_mg h, int variant)
+{
+  return guard([&] {
+    if (!h)
+      throw InvalidArg("null handle");
+    if (variant != PMG_GLOBAL && variant != PMG_SEPARATE && variant != PMG_FUSED &&
+        variant != PMG_BOUNDARY && variant != PMG_NAIVE)
+      throw InvalidArg("unknown smoother variant");
+    h->variant = variant;
+  });
+}
+
+int pmg_v_cycle(pmg_mg h, int li, void *x, const void *b, int use_graph, void *stream)
+{
+  return guard([&] {
+    if (!h || li < 0 || li >= static_cast<int>(h->levels.size()))
+      throw InvalidArg("v_cycle: level index out of range");
+    DeviceGuard dg(h->device);
+    PMG_DISPATCH_T(h, vcycle_entry<T>(h, li, static_cast<T *>(x), static_cast<const T *>(b),
+                                      use_graph != 0, as_stream(stream)));
+  });
+}
+
+int pmg_v_cycle_host(pmg_mg h, int li, void *x, const void *b)
+{
+  return guard([&] {
+    if (!h || li < 0 || li >= static_cast<int>(h->levels.size()))
+      throw InvalidArg("v_cycle: level index out of range");
+    DeviceGuard dg(h->device);
+    pmg_level_s *l = h->levels[li];
+    HostIO io(l);
+    const size_t bytes = static_cast<size_t>(l->S.N) * l->tsize;
+    void *dx = io.dev(0, bytes), *db = io.dev(1, bytes);
+    io.h2d(dx, x, bytes);
+    io.h2d(db, b, bytes);
+    PMG_DISPATCH_T(h, vcycle_impl<T>(h, li, static_cast<T *>(dx), static_cast<const T *>(db),
+                                     l->io_stream));
+    io.d2h(x, dx, bytes);
+    io.sync();
+  });
+}
+
+int pmg_full_multigrid(pmg_mg h, const void *const *rhs, void *x, double tol, int max_iterations,
+                       int *iterations, double *history, int history_cap, void *stream)
+{
+  return guard([&] {
+    if (!h)
+      throw InvalidArg("null handle");
+    if (h->dtype != PMG_F64)
+      throw InvalidArg("full_multigrid runs in f64 only (multigrid.hpp:80)");
+    if (!(tol > 0.0))
+      throw InvalidArg("full_multigrid: tol must be positive");
+    if (!rhs || !x)
+      throw InvalidArg("full_multigrid: null pointer");
+    DeviceGuard dg(h->device);
+    cudaStream_t s = as_stream(stream);
+    const int L = static_cast<int>(h->levels.size()) - 1;
+    using T = double;
+    // nested iteration (multigrid.cpp:366-377)
+    std::vector<T *> xl(L + 1);
+    for (int li = 0; li < L; ++li)
+    {
+      h->fmg_x[li].ensure(static_cast<size_t>(h->levels[li]->S.N) * sizeof(T));
+      xl[li] = h->fmg_x[li].as<T>();
+    }
+    xl[L] = static_cast<T *>(x);
+    vcycle_impl<T>(h, 0, xl[0], static_cast<const T *>(rhs[0]), s);
+    for (int li = 1; li <= L; ++li)
+    {
+      prolongate_impl<T>(h->levels[li - 1], h->levels[li], xl[li - 1], xl[li], false, s);
+      vcycle_impl<T>(h, li, xl[li], static_cast<const T *>(rhs[li]), s);
+    }
+    pmg_level_s *top = h->levels[L];
+    const T *bL = static_cast<const T *>(rhs[L]);
+    const double delta0 = norm_impl<T>(top, bL, top->S.N, s);
+    int it = 0;
+    int nh = 0;
+    if (history && history_cap > nh)
+      history[nh] = delta0;
+    ++nh;
+    double delta = delta0;
+    T *r = h->r_ws[L]->as<T>();
+    if (L == 0)
+    {
+      h->r_ws[0]->ensure(static_cast<size_t>(top->S.N) * sizeof(T));
+      r = h->r_ws[0]->as<T>();
+    }
+    while (delta > tol * delta0)
+    {
+      if (it >= max_iterations)
+      {
+        if (iterations)
+          *iterations = it;
+        throw Divergence("full_multigrid: no convergence after " + std::to_string(max_iterations) +
+                         " V-cycles");
+      }
+      vcycle_impl<T>(h, L, static_cast<T *>(x), bL, s);
+      ktab<T>(top).level_op(top->band_mats.data(), static_cast<const T *>(x), bL, r, top->S.m,
+                            top->sm_count, s);
+      delta = norm_impl<T>(top, r, top->S.N, s);
+      if (history && history_cap > nh)
+        history[nh] = delta;
+      ++nh;
+      ++it;
+    }
+    if (iterations)
+      *iterations = it;
+  });
+}
+
+int pmg_compute_rhs_host(int dim, int degree, int level, int kind, double *out)
+{
+  return guard([&] {
+    if (dim != 2 && dim != 3)
+      throw InvalidArg("dim must be 2 or 3");
+    auto b = compute_rhs(dim, degree, level, kind);
+    std::memcpy(out, b.data(), b.size() * sizeof(double));
+  });
+}
+
+int pmg_l2_error_sin_host(int dim, int degree, int level, const double *x, double *out)
+{
+  return guard([&] { *out = l2_error_sin(dim, degree, level, x); });
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// Internal state behind the C-ABI handles (shared by capi.cu and gmres.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pmg_b200.h"
+#include "common.cuh"
+#include "setup.hpp"
+
+namespace pmgb
+{
+
+struct DivergenceErr : std::runtime_error
+{
+  using std::runtime_error::runtime_error;
+};
+
+// RAII device buffer
+struct DevBuf
+{
+  void *p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  ~DevBuf()
+  {
+    if (p)
+      cudaFree(p);
+  }
+  void ensure(size_t b)
+  {
+    if (b <= bytes)
+      return;
+    if (p)
+      check_cuda(cudaFree(p), "cudaFree");
+    p = nullptr;
+    bytes = 0;
+    check_cuda(cudaMalloc(&p, b), "cudaMalloc");
+    bytes = b;
+  }
+  template <typename T>
+  T *as() const
+  {
+    return static_cast<T *>(p);
+  }
+};
+
+struct DevScope
+{
+  int prev = 0;
+  explicit DevScope(int dev)
+  {
+    check_cuda(cudaGetDevice(&prev), "cudaGetDevice");
+    if (prev != dev)
+      check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DevScope() { cudaSetDevice(prev); }
+};
+
+struct GmresWork
+{
+  DevBuf bV, bZ, bw, br, bred, brf, bzf, bflag;
+  double *V = nullptr, *Z = nullptr, *w = nullptr, *r = nullptr, *red = nullptr;
+  float *rf = nullptr, *zf = nullptr;
+  int *flag = nullptr;
+  void ensure(int64_t n, int restart, bool mixed);
+};
+
+// maps C++ exceptions to pmg_status and records pmg_last_error
+int capi_status_from_current_exception();
+
+template <typename F>
+int capi_guard(F &&f)
+{
+  try
+  {
+    f();
+    return PMG_OK;
+  }
+  catch (...)
+  {
+    return capi_status_from_current_exception();
+  }
+}
+
+int mg_dtype(pmg_mg h);
+int mg_device(pmg_mg h);
+int mg_levels(pmg_mg h);
+pmg_level mg_level_ptr(pmg_mg h, int li);
+int64_t level_total(pmg_level l);
+int level_sm_count(pmg_level l);
+GmresWork &mg_gmres_work(pmg_mg h);
+void mg_apply_finest_op(pmg_mg h, const double *x, double *y, cudaStream_t s);
+void mg_residual_finest(pmg_mg h, const double *x, const double *b, double *r, cudaStream_t s);
+void mg_vcycle_f32(pmg_mg h, int li, float *x, const float *b, cudaStream_t s);
+void mg_vcycle_f64(pmg_mg h, int li, double *x, const double *b, cudaStream_t s);
+
+}  // namespace pmgb

@@ -1,0 +1,102 @@
+// Shared device-side definitions of the B200 vertex-patch multigrid library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace pmgb
+{
+
+// ---------------------------------------------------------------------------
+// errors / launch accounting
+// ---------------------------------------------------------------------------
+
+struct CudaError : std::runtime_error
+{
+  using std::runtime_error::runtime_error;
+};
+
+inline void check_cuda(cudaError_t e, const char *what)
+{
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void note_launch(int n = 1);       // counts kernel launches (pmg_launch_count)
+void check_launch(const char *what);  // cudaGetLastError + count
+
+// true the first time it is called for the current device with this mask
+// (per-function attribute setup such as the dynamic shared-memory limit)
+inline bool first_on_device(unsigned &mask)
+{
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned bit = 1u << (dev & 31);
+  if (mask & bit)
+    return false;
+  mask |= bit;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// per-level constant data passed BY VALUE as kernel parameters
+// (__grid_constant__). With K a template parameter every matrix entry is a
+// compile-time offset into the parameter bank, so the contractions issue
+// DFMA/FFMA with uniform-register operands and no shared-memory or
+// constant-cache traffic for the 1D matrices.
+// ---------------------------------------------------------------------------
+
+template <typename T, int K>
+struct PatchMats
+{
+  static constexpr int NC = 2 * K + 1;  // closure points per direction
+  static constexpr int NI = 2 * K - 1;  // interior points per direction
+  T M[NI][NC];  // interior rows of the two-cell mass matrix      (fastdiag.hpp:30 mass_if)
+  T A[NI][NC];  // interior rows of the two-cell stiffness matrix (fastdiag.hpp:30 stiff_if)
+  T S[NI][NI];  // generalized eigenvectors, columns              (fastdiag.hpp:52)
+};
+
+// Rows of the global 1D matrices by lattice residue r = p mod K, offsets
+// o = q - p + K in [0, 2K]; the level operator is their Kronecker sum.
+template <typename T, int K>
+struct BandMats
+{
+  T M[K][2 * K + 1];
+  T A[K][2 * K + 1];
+};
+
+// (2K+1) x (K+1) embedding of the coarse cell basis into its two fine cells
+// (level_context.cpp:21-34).
+template <typename T, int K>
+struct ProlMats
+{
+  T P[2 * K + 1][K + 1];
+};
+
+// Smoother modes (one kernel template, four organisations of the reference's
+// SmootherVariant, smoother.cpp:61-149).
+enum : int
+{
+  MODE_FUSED = 0,     // residual + solve + x += v          (variant fused)
+  MODE_BOUNDARY = 1,  // never reads x^I, x^I = v           (variant boundary)
+  MODE_RESIDUAL = 2,  // r^I = b^I - A x, to a global buffer (separate, pass 1)
+  MODE_SOLVE = 3      // v = A_j^{-1} r^I from global, x += v (separate pass 2 / global)
+};
+
+template <typename T>
+struct ColorArgs
+{
+  T *x;           // level vector (updated)
+  const T *b;     // right-hand side
+  T *r;           // global residual buffer (MODE_RESIDUAL output / MODE_SOLVE input)
+  const T *inv;   // inverse eigenvalue sums, (2K-1)^D, direction 0 fastest
+  int64_t m;      // dofs per direction
+  int np[3];      // patches of this colour per direction
+  int vb[3];      // vertex coordinate v_a = 2 j_a + vb[a]
+  int total;      // patches in this colour
+};
+
+}  // namespace pmgb

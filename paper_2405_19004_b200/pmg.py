@@ -1,0 +1,540 @@
+"""Python host mirror of the reference `pmg` interface, over the C-ABI.
+
+Same names, argument meaning and error behaviour as /root/reference/proj/
+include/pmg/*.hpp (the parity tests read like the SPEC's examples):
+
+  build_hierarchy / dof_index / CartesianLevel     mesh.hpp:16-35
+  make_level_context / LevelContext                level_context.hpp:17-29
+  make_multigrid_context / MultigridContext        multigrid.hpp:34-54
+  smooth                                           smoother.hpp:45-47
+  apply_laplacian / compute_rhs / l2_error         operator.hpp:47-64
+  prolongate / restrict_vector                     multigrid.hpp:56-63
+  v_cycle / full_multigrid / FmgStats              multigrid.hpp:68-86
+  vector_norm / compute_residual                   multigrid.hpp:89-92
+  gmres / SolveStats (+ mixed precision)           krylov.hpp:16-39
+  DivergenceError                                  multigrid.hpp:22-29
+
+Vectors are either torch CUDA tensors (device path: the C-ABI enqueues on the
+current torch stream, x is updated in place) or numpy arrays (host path: the
+*_host C-ABI entry points copy in, compute on the GPU, copy out). Every
+computation runs in the CUDA library; nothing here does arithmetic on the
+vectors.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import PMG_F32, PMG_F64, VARIANTS, DivergenceError, check
+
+__all__ = [
+    "CartesianLevel", "build_hierarchy", "dof_index", "LevelContext", "make_level_context",
+    "MultigridContext", "make_multigrid_context", "SmootherVariant", "smooth", "smooth_color",
+    "apply_laplacian", "compute_residual", "prolongate", "restrict_vector", "v_cycle",
+    "full_multigrid", "FmgStats", "vector_norm", "compute_rhs", "l2_error", "gmres", "SolveStats",
+    "DivergenceError",
+]
+
+
+class SmootherVariant:
+    """smoother.hpp:21-27 (+ the straightforward global-memory comparator)."""
+
+    global_ = "global"
+    separate = "separate"
+    fused = "fused"
+    boundary = "boundary"
+    naive = "naive"
+
+
+# ---------------------------------------------------------------------------
+# mesh (mesh.hpp)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class CartesianLevel:
+    level: int = 1
+    dim: int = 2
+    degree: int = 1
+
+    @property
+    def cells_per_dim(self) -> int:
+        return 1 << self.level
+
+    @property
+    def dofs_per_dim(self) -> int:
+        return self.cells_per_dim * self.degree - 1
+
+    @property
+    def spacing(self) -> float:
+        return 1.0 / self.cells_per_dim
+
+    @property
+    def total_dofs(self) -> int:
+        return self.dofs_per_dim ** self.dim
+
+
+def build_hierarchy(dim: int, degree: int, finest_level: int) -> list[CartesianLevel]:
+    if dim not in (2, 3):
+        raise ValueError(f"build_hierarchy: dim must be 2 or 3, got {dim}")
+    if degree < 1:
+        raise ValueError("build_hierarchy: degree must be >= 1")
+    if finest_level < 1:
+        raise ValueError("build_hierarchy: finest_level must be >= 1")
+    return [CartesianLevel(l, dim, degree) for l in range(1, finest_level + 1)]
+
+
+def dof_index(level: CartesianLevel, multi_index) -> int:
+    if len(multi_index) != level.dim:
+        raise ValueError("dof_index: multi-index size does not match dim")
+    m = level.dofs_per_dim
+    idx, stride = 0, 1
+    for a, v in enumerate(multi_index):
+        if not 0 <= v < m:
+            raise IndexError(f"dof_index: component {a} out of range")
+        idx += v * stride
+        stride *= m
+    return idx
+
+
+# ---------------------------------------------------------------------------
+# array plumbing
+# ---------------------------------------------------------------------------
+
+
+def _dtype_code(dtype) -> int:
+    dt = np.dtype(dtype)
+    if dt == np.float64:
+        return PMG_F64
+    if dt == np.float32:
+        return PMG_F32
+    raise ValueError(f"unsupported dtype {dtype} (float32 / float64 only)")
+
+
+def _is_torch(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
+class _Arr:
+    """Classifies an argument as a device (torch CUDA) or host (numpy) array."""
+
+    def __init__(self, a, n: int, dtype_code: int, name: str, writable: bool):
+        if _is_torch(a):
+            import torch
+
+            if not a.is_cuda:
+                raise ValueError(f"{name}: torch tensors must live on a CUDA device")
+            want = torch.float64 if dtype_code == PMG_F64 else torch.float32
+            if a.dtype != want:
+                raise ValueError(f"{name}: dtype {a.dtype} does not match the context ({want})")
+            if not a.is_contiguous():
+                raise ValueError(f"{name}: tensor must be contiguous")
+            if a.numel() != n:
+                raise ValueError(f"{name}: vector size does not match level")
+            self.device = True
+            self.ptr = ctypes.c_void_p(a.data_ptr())
+            self.obj = a
+        else:
+            if not isinstance(a, np.ndarray):
+                raise TypeError(f"{name}: expected a numpy array or a torch CUDA tensor")
+            want = np.float64 if dtype_code == PMG_F64 else np.float32
+            if a.dtype != want:
+                raise ValueError(f"{name}: dtype {a.dtype} does not match the context ({np.dtype(want)})")
+            if a.size != n:
+                raise ValueError(f"{name}: vector size does not match level")
+            if not a.flags.c_contiguous or (writable and not a.flags.writeable):
+                raise ValueError(f"{name}: array must be C-contiguous (and writable)")
+            self.device = False
+            self.ptr = ctypes.c_void_p(a.ctypes.data)
+            self.obj = a
+
+
+def _stream(arrs) -> ctypes.c_void_p:
+    import torch
+
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _same_kind(*arrs):
+    kinds = {a.device for a in arrs}
+    if len(kinds) != 1:
+        raise ValueError("mix of host (numpy) and device (torch) vectors")
+    return kinds.pop()
+
+
+# ---------------------------------------------------------------------------
+# level context
+# ---------------------------------------------------------------------------
+
+
+class LevelContext:
+    """Per-level immutable setup (level_context.hpp:17-26), resident on the GPU."""
+
+    def __init__(self, handle, level: CartesianLevel, dtype, device: int, owner=None):
+        self._h = ctypes.c_void_p(handle)
+        self.level = level
+        self.dtype = np.dtype(dtype)
+        self.device = device
+        self._owner = owner  # keeps a MultigridContext alive for borrowed levels
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def _code(self):
+        return _dtype_code(self.dtype)
+
+    def setup_data(self) -> dict:
+        """The f64 setup uploaded for this level (for parity tests)."""
+        k, d = self.level.degree, self.level.dim
+        ni, nc = 2 * k - 1, 2 * k + 1
+        out = {
+            "S": np.zeros((ni, ni)), "lambda": np.zeros(ni), "mass_if": np.zeros((ni, nc)),
+            "stiff_if": np.zeros((ni, nc)), "prolongation": np.zeros((nc, k + 1)),
+            "cell_mass": np.zeros((k + 1, k + 1)), "cell_stiffness": np.zeros((k + 1, k + 1)),
+        }
+        P = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+        check(_lib.load().pmg_level_setup_data(
+            self._h, P(out["S"]), P(out["lambda"]), P(out["mass_if"]), P(out["stiff_if"]),
+            P(out["prolongation"]), P(out["cell_mass"]), P(out["cell_stiffness"])), "setup_data")
+        return out
+
+    def __del__(self):
+        if self._owner is None and getattr(self, "_h", None) and _lib._lib is not None:
+            _lib._lib.pmg_level_destroy(self._h)
+            self._h = None
+
+
+def make_level_context(level: CartesianLevel, dtype=np.float64, device: int = 0) -> LevelContext:
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    check(lib.pmg_level_create(level.dim, level.degree, level.level, _dtype_code(dtype), device,
+                               ctypes.byref(h)), "make_level_context")
+    return LevelContext(h.value, level, dtype, device)
+
+
+# ---------------------------------------------------------------------------
+# smoother / operator / transfers
+# ---------------------------------------------------------------------------
+
+
+def _variant_code(variant) -> int:
+    if isinstance(variant, int):
+        return variant
+    try:
+        return VARIANTS[variant]
+    except KeyError:
+        raise ValueError(f"unknown smoother variant {variant!r}") from None
+
+
+def smooth(ctx: LevelContext, x, b, variant="fused", threads: int = 1, ws=None) -> None:
+    """One colourised multiplicative vertex-patch step, x updated in place
+    (smoother.hpp:45-47). `threads`/`ws` are accepted for signature parity;
+    the GPU grid replaces parallel_for."""
+    n = ctx.level.total_dofs
+    xa = _Arr(x, n, ctx._code, "x", True)
+    ba = _Arr(b, n, ctx._code, "b", False)
+    v = _variant_code(variant)
+    lib = _lib.load()
+    if _same_kind(xa, ba):
+        check(lib.pmg_smooth(ctx.handle, v, xa.ptr, ba.ptr, _stream((xa, ba))), "smooth")
+    else:
+        check(lib.pmg_smooth_host(ctx.handle, v, xa.ptr, ba.ptr), "smooth")
+
+
+def smooth_color(ctx: LevelContext, color: int, x, b, variant="fused") -> None:
+    """One colour of a smoothing step (device vectors only)."""
+    n = ctx.level.total_dofs
+    xa = _Arr(x, n, ctx._code, "x", True)
+    ba = _Arr(b, n, ctx._code, "b", False)
+    if not (xa.device and ba.device):
+        raise ValueError("smooth_color: device (torch CUDA) vectors only")
+    check(_lib.load().pmg_smooth_color(ctx.handle, _variant_code(variant), color, xa.ptr, ba.ptr,
+                                       _stream((xa, ba))), "smooth_color")
+
+
+def apply_laplacian(ctx: LevelContext, x, y, mode: str = "colored", threads: int = 1) -> None:
+    """y = A_l x (operator.hpp:47-50)."""
+    n = ctx.level.total_dofs
+    xa = _Arr(x, n, ctx._code, "x", False)
+    ya = _Arr(y, n, ctx._code, "y", True)
+    lib = _lib.load()
+    if _same_kind(xa, ya):
+        check(lib.pmg_apply_laplacian(ctx.handle, xa.ptr, ya.ptr, _stream((xa, ya))), "apply_laplacian")
+    else:
+        check(lib.pmg_apply_laplacian_host(ctx.handle, xa.ptr, ya.ptr), "apply_laplacian")
+
+
+def compute_residual(ctx: LevelContext, x, b, r, threads: int = 1) -> None:
+    """r = b - A x (multigrid.hpp:90-92)."""
+    n = ctx.level.total_dofs
+    xa = _Arr(x, n, ctx._code, "x", False)
+    ba = _Arr(b, n, ctx._code, "b", False)
+    ra = _Arr(r, n, ctx._code, "r", True)
+    lib = _lib.load()
+    if _same_kind(xa, ba, ra):
+        check(lib.pmg_compute_residual(ctx.handle, xa.ptr, ba.ptr, ra.ptr, _stream((xa,))), "compute_residual")
+    else:
+        check(lib.pmg_compute_residual_host(ctx.handle, xa.ptr, ba.ptr, ra.ptr), "compute_residual")
+
+
+def _check_pair(coarse: LevelContext, fine: LevelContext, what: str):
+    cl, fl = coarse.level, fine.level
+    if fl.level != cl.level + 1 or fl.degree != cl.degree or fl.dim != cl.dim:
+        raise ValueError(f"{what}: levels are not consecutive")
+
+
+def prolongate(coarse: LevelContext, fine: LevelContext, x_coarse, x_fine, accumulate: bool = False) -> None:
+    """x_fine = P x_coarse (multigrid.hpp:56-58); accumulate gives +=."""
+    _check_pair(coarse, fine, "prolongate")
+    xc = _Arr(x_coarse, coarse.level.total_dofs, fine._code, "x_coarse", False)
+    xf = _Arr(x_fine, fine.level.total_dofs, fine._code, "x_fine", True)
+    lib = _lib.load()
+    if _same_kind(xc, xf):
+        check(lib.pmg_prolongate(coarse.handle, fine.handle, xc.ptr, xf.ptr, int(accumulate),
+                                 _stream((xc,))), "prolongate")
+    else:
+        if accumulate:
+            raise ValueError("prolongate: accumulate needs device vectors")
+        check(lib.pmg_prolongate_host(coarse.handle, fine.handle, xc.ptr, xf.ptr), "prolongate")
+
+
+def restrict_vector(coarse: LevelContext, fine: LevelContext, r_fine, r_coarse) -> None:
+    """r_coarse = P^T r_fine (multigrid.hpp:61-63)."""
+    _check_pair(coarse, fine, "restrict_vector")
+    rf = _Arr(r_fine, fine.level.total_dofs, fine._code, "r_fine", False)
+    rc = _Arr(r_coarse, coarse.level.total_dofs, fine._code, "r_coarse", True)
+    lib = _lib.load()
+    if _same_kind(rf, rc):
+        check(lib.pmg_restrict_vector(coarse.handle, fine.handle, rf.ptr, rc.ptr, _stream((rf,))),
+              "restrict_vector")
+    else:
+        check(lib.pmg_restrict_vector_host(coarse.handle, fine.handle, rf.ptr, rc.ptr), "restrict_vector")
+
+
+def vector_norm(v, device: int = 0) -> float:
+    """Euclidean norm (multigrid.cpp:260-266), deterministic device reduction."""
+    lib = _lib.load()
+    out = ctypes.c_double()
+    if _is_torch(v):
+        code = _dtype_code(str(v.dtype).replace("torch.", ""))
+        a = _Arr(v, v.numel(), code, "v", False)
+        check(lib.pmg_norm2(a.ptr, v.numel(), code, v.device.index or 0, ctypes.byref(out),
+                            _stream((a,))), "vector_norm")
+        return out.value
+    import torch  # host vector: stage through the device like every other op
+
+    t = torch.from_numpy(np.ascontiguousarray(v)).to(f"cuda:{device}")
+    return vector_norm(t)
+
+
+# ---------------------------------------------------------------------------
+# multigrid context / V-cycle / FMG
+# ---------------------------------------------------------------------------
+
+
+class MultigridContext:
+    """Level hierarchy + device workspaces (multigrid.hpp:34-49). Index 0 is
+    mesh level 1 (one interior vertex)."""
+
+    def __init__(self, handle, dim, degree, finest_level, variant, dtype, device):
+        self._h = ctypes.c_void_p(handle)
+        self.dtype = np.dtype(dtype)
+        self.device = device
+        self._variant = variant
+        self._pre, self._post = 1, 1
+        lib = _lib.load()
+        self.levels = [
+            LevelContext(lib.pmg_mg_level(self._h, li), lev, dtype, device, owner=self)
+            for li, lev in enumerate(build_hierarchy(dim, degree, finest_level))
+        ]
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def variant(self):
+        return self._variant
+
+    @variant.setter
+    def variant(self, v):
+        check(_lib.load().pmg_mg_set_variant(self._h, _variant_code(v)), "variant")
+        self._variant = v
+
+    @property
+    def pre_smooth(self):
+        return self._pre
+
+    @pre_smooth.setter
+    def pre_smooth(self, n):
+        check(_lib.load().pmg_mg_set_smoothing(self._h, int(n), self._post), "pre_smooth")
+        self._pre = int(n)
+
+    @property
+    def post_smooth(self):
+        return self._post
+
+    @post_smooth.setter
+    def post_smooth(self, n):
+        check(_lib.load().pmg_mg_set_smoothing(self._h, self._pre, int(n)), "post_smooth")
+        self._post = int(n)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            _lib._lib.pmg_mg_destroy(self._h)
+            self._h = None
+
+
+def make_multigrid_context(dim: int, degree: int, finest_level: int, variant="fused",
+                           kind: str = "vertex_patch", threads: int = 1, dtype=np.float64,
+                           device: int = 0) -> MultigridContext:
+    """multigrid.hpp:51-54. kind must be vertex_patch (point Gauss-Seidel is
+    out of scope)."""
+    if kind != "vertex_patch":
+        raise ValueError("only the vertex-patch smoother is provided on the GPU")
+    build_hierarchy(dim, degree, finest_level)  # same argument validation
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    check(lib.pmg_mg_create(dim, degree, finest_level, _dtype_code(dtype), _variant_code(variant),
+                            device, ctypes.byref(h)), "make_multigrid_context")
+    return MultigridContext(h.value, dim, degree, finest_level, variant, dtype, device)
+
+
+def v_cycle(ctx: MultigridContext, li: int, x, b, use_graph: bool = False) -> None:
+    """One V-cycle on level index li (multigrid.hpp:68-69), x in place."""
+    if not 0 <= li < len(ctx.levels):
+        raise ValueError("v_cycle: level index out of range")
+    lev = ctx.levels[li]
+    n = lev.level.total_dofs
+    xa = _Arr(x, n, lev._code, "x", True)
+    ba = _Arr(b, n, lev._code, "b", False)
+    lib = _lib.load()
+    if _same_kind(xa, ba):
+        check(lib.pmg_v_cycle(ctx.handle, li, xa.ptr, ba.ptr, int(use_graph), _stream((xa,))), "v_cycle")
+    else:
+        check(lib.pmg_v_cycle_host(ctx.handle, li, xa.ptr, ba.ptr), "v_cycle")
+
+
+@dataclass
+class FmgStats:
+    """multigrid.hpp:74-78."""
+
+    iterations: int = 0
+    residual_history: list = field(default_factory=list)
+
+
+def full_multigrid(ctx: MultigridContext, rhs_per_level, x, tol: float, max_iterations: int = 100) -> FmgStats:
+    """Alg. 2 (multigrid.hpp:80-86): nested iteration then V-cycles until
+    ||b - A x|| <= tol ||b||. f64 contexts only. Raises DivergenceError."""
+    import torch
+
+    if ctx.dtype != np.float64:
+        raise ValueError("full_multigrid: f64 contexts only")
+    if tol <= 0:
+        raise ValueError("full_multigrid: tol must be positive")
+    L = len(ctx.levels)
+    if len(rhs_per_level) != L:
+        raise ValueError("full_multigrid: need one rhs per level")
+    dev = f"cuda:{ctx.device}"
+    rhs_dev = [r if _is_torch(r) else torch.from_numpy(np.ascontiguousarray(r, dtype=np.float64)).to(dev)
+               for r in rhs_per_level]
+    for r, lev in zip(rhs_dev, ctx.levels):
+        _Arr(r, lev.level.total_dofs, PMG_F64, "rhs", False)
+    host_x = not _is_torch(x)
+    xd = torch.zeros(ctx.levels[-1].level.total_dofs, dtype=torch.float64, device=dev) if host_x else x
+    _Arr(xd, ctx.levels[-1].level.total_dofs, PMG_F64, "x", True)
+    ptrs = (ctypes.c_void_p * L)(*[r.data_ptr() for r in rhs_dev])
+    cap = max_iterations + 2
+    hist = np.full(cap, np.nan)
+    its = ctypes.c_int(0)
+    st = _lib.load().pmg_full_multigrid(
+        ctx.handle, ptrs, ctypes.c_void_p(xd.data_ptr()), float(tol), int(max_iterations), ctypes.byref(its),
+        hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap,
+        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    history = [float(h) for h in hist[: its.value + 1]]
+    check(st, "full_multigrid", history)
+    if host_x:
+        np.copyto(x, xd.cpu().numpy())
+    return FmgStats(its.value, history)
+
+
+def compute_rhs(level: CartesianLevel, f: str = "one") -> np.ndarray:
+    """b_i = int f phi_i (operator.hpp:58-59) for f = 1 ('one') or
+    f = d pi^2 prod sin(pi x_a) ('sin')."""
+    kinds = {"one": 0, "sin": 1}
+    if f not in kinds:
+        raise ValueError("compute_rhs: f must be 'one' or 'sin'")
+    out = np.zeros(level.total_dofs)
+    check(_lib.load().pmg_compute_rhs_host(level.dim, level.degree, level.level, kinds[f],
+                                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), "compute_rhs")
+    return out
+
+
+def l2_error(level: CartesianLevel, x, u_exact: str = "sin") -> float:
+    """L2 error against u = prod sin(pi x_a) (operator.hpp:62-64)."""
+    if u_exact != "sin":
+        raise ValueError("l2_error: only u = prod sin(pi x) is provided")
+    xh = x.detach().cpu().numpy() if _is_torch(x) else np.ascontiguousarray(x, dtype=np.float64)
+    xh = np.ascontiguousarray(xh, dtype=np.float64)
+    if xh.size != level.total_dofs:
+        raise ValueError("l2_error: vector size does not match level")
+    out = ctypes.c_double()
+    check(_lib.load().pmg_l2_error_sin_host(level.dim, level.degree, level.level,
+                                            xh.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                            ctypes.byref(out)), "l2_error")
+    return out.value
+
+
+# ---------------------------------------------------------------------------
+# Krylov (krylov.hpp)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class SolveStats:
+    iterations: int = 0
+    residual_history: list = field(default_factory=list)
+    l2_error: float | None = None
+    wall_seconds: float = 0.0
+
+
+def gmres(op_ctx: MultigridContext, prec_ctx: MultigridContext, b, x, tol: float, restart: int = 30,
+          max_iterations: int = 200) -> SolveStats:
+    """Right-preconditioned GMRES(restart) in f64 with one V-cycle of
+    `prec_ctx` as preconditioner: an f32 context is the paper's mixed
+    precision mode (krylov.cpp:152-171), an f64 context the double mode."""
+    import time
+
+    import torch
+
+    n = op_ctx.levels[-1].level.total_dofs
+    dev = f"cuda:{op_ctx.device}"
+    bd = b if _is_torch(b) else torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).to(dev)
+    host_x = not _is_torch(x)
+    xd = torch.zeros(n, dtype=torch.float64, device=dev) if host_x else x
+    _Arr(bd, n, PMG_F64, "b", False)
+    _Arr(xd, n, PMG_F64, "x", True)
+    cap = max_iterations + 8
+    hist = np.full(cap, np.nan)
+    its = ctypes.c_int(0)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    st = _lib.load().pmg_gmres(op_ctx.handle, prec_ctx.handle, ctypes.c_void_p(bd.data_ptr()),
+                               ctypes.c_void_p(xd.data_ptr()), float(tol), int(restart), int(max_iterations),
+                               ctypes.byref(its), hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap,
+                               ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - t0
+    h = [float(v) for v in hist if not np.isnan(v)]
+    if -1.0 in h:
+        h = h[: h.index(-1.0)]
+    check(st, "gmres", h)
+    if host_x:
+        np.copyto(x, xd.cpu().numpy())
+    return SolveStats(its.value, h, None, wall)

@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference
+library compiled from /root/reference (oracle/_ref) on the same seeded inputs.
+
+Tolerances (BASELINE.json north star): f64 relative 1e-12 on smoother output,
+operator/residual, transfers and V-cycle; f32 relative 1e-5 (residuals
+relative to ||b||, SURVEY.md §7 "FP32 parity definition"); FMG iteration
+counts identical at a 1e-8 reduction.
+"""
+
+import numpy as np
+import pytest
+
+import refbind
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float64: 1e-12, np.float32: 1e-5}
+
+# (dim, degree, finest level): every degree 1..7 in 2D and 3D at sizes the
+# reference finishes in well under a second
+CASES = [
+    (2, 1, 5), (2, 2, 6), (2, 3, 4), (2, 4, 4), (2, 5, 3), (2, 6, 3), (2, 7, 3),
+    (3, 1, 4), (3, 2, 4), (3, 3, 3), (3, 4, 3), (3, 5, 2), (3, 6, 2), (3, 7, 2),
+]
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a, np.float64) - np.asarray(b, np.float64)) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def pmg(cuda):
+    import paper_2405_19004_b200 as p
+
+    if not refbind.available():
+        pytest.fail("oracle/_ref/libpmg_ref.so missing: run __graft_entry__.build() where /root/reference exists")
+    return p
+
+
+def inputs(n, dtype, seed=42):
+    x, b = refbind.fill_uniform(seed, n, n)
+    return x.astype(dtype), b.astype(dtype)
+
+
+def dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")
+def test_smoother_variants(pmg, cuda, case, dtype):
+    dim, k, L = case
+    ref = refbind.RefMg(dim, k, L, prec=0 if dtype == np.float64 else 1)
+    ctx = pmg.make_multigrid_context(dim, k, L, dtype=dtype)
+    lev = ctx.levels[-1]
+    x0, b = inputs(lev.level.total_dofs, dtype)
+    want = ref.smooth(L - 1, x0, b, "fused")
+    for variant in ["fused", "boundary", "separate", "global", "naive"]:
+        xd = dev(cuda, x0.copy())
+        pmg.smooth(lev, xd, dev(cuda, b), variant)
+        got = xd.cpu().numpy()
+        assert rel(got, want) < TOL[dtype], (variant, rel(got, want))
+        if variant != "naive":
+            want_v = ref.smooth(L - 1, x0, b, variant)
+            assert rel(got, want_v) < TOL[dtype], (variant, rel(got, want_v))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")
+def test_operator_and_residual(pmg, cuda, case, dtype):
+    dim, k, L = case
+    ref = refbind.RefMg(dim, k, L, prec=0 if dtype == np.float64 else 1)
+    ctx = pmg.make_multigrid_context(dim, k, L, dtype=dtype)
+    lev = ctx.levels[-1]
+    x0, b = inputs(lev.level.total_dofs, dtype)
+    y = cuda.zeros_like(dev(cuda, x0))
+    pmg.apply_laplacian(lev, dev(cuda, x0), y)
+    want = ref.apply_laplacian(L - 1, x0)
+    assert rel(y.cpu().numpy(), want) < TOL[dtype]
+    r = cuda.zeros_like(y)
+    pmg.compute_residual(lev, dev(cuda, x0), dev(cuda, b), r)
+    want = ref.residual(L - 1, x0, b)
+    err = np.linalg.norm(r.cpu().numpy().astype(np.float64) - want) / np.linalg.norm(b.astype(np.float64))
+    assert err < TOL[dtype]
+    if dtype == np.float64:
+        assert rel(r.cpu().numpy(), want) < 1e-12
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")
+def test_transfers(pmg, cuda, case, dtype):
+    dim, k, L = case
+    if L < 2:
+        pytest.skip("needs two levels")
+    ref = refbind.RefMg(dim, k, L, prec=0 if dtype == np.float64 else 1)
+    ctx = pmg.make_multigrid_context(dim, k, L, dtype=dtype)
+    c, f = ctx.levels[-2], ctx.levels[-1]
+    xc, _ = inputs(c.level.total_dofs, dtype, seed=7)
+    rf, _ = inputs(f.level.total_dofs, dtype, seed=9)
+    xf = cuda.zeros(f.level.total_dofs, dtype=cuda.float64 if dtype == np.float64 else cuda.float32, device="cuda")
+    pmg.prolongate(c, f, dev(cuda, xc), xf)
+    assert rel(xf.cpu().numpy(), ref.prolongate(L - 2, xc)) < TOL[dtype]
+    rc = cuda.zeros(c.level.total_dofs, dtype=xf.dtype, device="cuda")
+    pmg.restrict_vector(c, f, dev(cuda, rf), rc)
+    assert rel(rc.cpu().numpy(), ref.restrict(L - 2, rf)) < TOL[dtype]
+    # accumulate form used by the V-cycle: x += P xc
+    base = dev(cuda, rf.copy())
+    pmg.prolongate(c, f, dev(cuda, xc), base, accumulate=True)
+    assert rel(base.cpu().numpy(), rf.astype(np.float64) + ref.prolongate(L - 2, xc)) < TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")
+def test_vcycle(pmg, cuda, case, dtype):
+    dim, k, L = case
+    ref = refbind.RefMg(dim, k, L, prec=0 if dtype == np.float64 else 1)
+    ctx = pmg.make_multigrid_context(dim, k, L, dtype=dtype)
+    lev = ctx.levels[-1]
+    x0, b = inputs(lev.level.total_dofs, dtype)
+    want = ref.vcycle(L - 1, x0, b)
+    for use_graph in (False, True):
+        xd = dev(cuda, x0.copy())
+        pmg.v_cycle(ctx, L - 1, xd, dev(cuda, b), use_graph=use_graph)
+        assert rel(xd.cpu().numpy(), want) < (1e-11 if dtype == np.float64 else 1e-4)
+
+
+@pytest.mark.parametrize("case", [(2, 1, 4), (2, 2, 6), (2, 3, 4), (3, 1, 4), (3, 2, 4), (3, 3, 3), (3, 4, 3)],
+                         ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")
+@pytest.mark.parametrize("rhs", [0, 1], ids=["one", "sin"])
+def test_fmg_iteration_counts(pmg, cuda, case, rhs):
+    dim, k, L = case
+    ref = refbind.RefMg(dim, k, L)
+    st, xref, it_ref, hist_ref = ref.fmg(rhs, 1e-8)
+    assert st == 0
+    ctx = pmg.make_multigrid_context(dim, k, L)
+    rl = [refbind.compute_rhs(dim, k, l, rhs) for l in range(1, L + 1)]
+    x = cuda.zeros(ctx.levels[-1].level.total_dofs, dtype=cuda.float64, device="cuda")
+    stats = pmg.full_multigrid(ctx, rl, x, 1e-8)
+    assert stats.iterations == it_ref
+    # histories agree to rounding; entries near machine precision relative to ||b||
+    assert np.allclose(stats.residual_history, hist_ref, rtol=1e-6, atol=1e-9 * hist_ref[0])
+    assert rel(x.cpu().numpy(), xref) < 1e-11
+
+
+@pytest.mark.parametrize("dim,k", [(2, 1), (2, 4), (3, 2), (3, 7)])
+def test_level1_exact_solve(pmg, cuda, dim, k):
+    """on level 1 one smoothing step solves A x = b exactly."""
+    ctx = pmg.make_multigrid_context(dim, k, 1)
+    lev = ctx.levels[0]
+    n = lev.level.total_dofs
+    _, b = inputs(n, np.float64)
+    x = cuda.zeros(n, dtype=cuda.float64, device="cuda")
+    bd = dev(cuda, b)
+    pmg.smooth(lev, x, bd)
+    r = cuda.zeros_like(x)
+    pmg.compute_residual(lev, x, bd, r)
+    assert r.norm().item() <= 1e-10 * np.linalg.norm(b)
+
+
+def test_survey_goldens(pmg, cuda):
+    """SURVEY.md §8c golden norms for C1 (2D Q2 L=6), mt19937_64(42) inputs."""
+    ctx = pmg.make_multigrid_context(2, 2, 6)
+    lev = ctx.levels[-1]
+    x0, b = inputs(lev.level.total_dofs, np.float64)
+    assert abs(np.linalg.norm(x0) - 72.91594658921915) < 1e-10
+    xd, bd = dev(cuda, x0.copy()), dev(cuda, b)
+    r = cuda.zeros_like(xd)
+    pmg.compute_residual(lev, xd, bd, r)
+    assert abs(r.norm().item() - 338.1620349001778) < 1e-9
+    pmg.smooth(lev, xd, bd)
+    assert abs(xd.norm().item() - 43.49331532632719) < 1e-10
+    pmg.compute_residual(lev, xd, bd, r)
+    assert abs(r.norm().item() - 21.67284987997918) < 1e-9
+    xd = dev(cuda, x0.copy())
+    pmg.v_cycle(ctx, 5, xd, bd)
+    assert abs(xd.norm().item() - 783.2195575549429) < 1e-8
+    pmg.compute_residual(lev, xd, bd, r)
+    assert abs(r.norm().item() - 0.7452650912722393) < 1e-9
+
+
+def test_host_buffer_entry_points(pmg, cuda):
+    """numpy (host) vectors go through the *_host C-ABI calls (H2D, kernel, D2H)."""
+    dim, k, L = 3, 3, 3
+    ref = refbind.RefMg(dim, k, L)
+    ctx = pmg.make_multigrid_context(dim, k, L)
+    lev = ctx.levels[-1]
+    x0, b = inputs(lev.level.total_dofs, np.float64)
+    x = x0.copy()
+    pmg.smooth(lev, x, b)
+    assert rel(x, ref.smooth(L - 1, x0, b)) < 1e-12
+    y = np.zeros_like(x0)
+    pmg.apply_laplacian(lev, x0, y)
+    assert rel(y, ref.apply_laplacian(L - 1, x0)) < 1e-12
+    x = x0.copy()
+    pmg.v_cycle(ctx, L - 1, x, b)
+    assert rel(x, ref.vcycle(L - 1, x0, b)) < 1e-11
+
+
+def test_determinism(pmg, cuda):
+    """No atomics anywhere: two runs are bitwise identical."""
+    ctx = pmg.make_multigrid_context(3, 4, 3)
+    lev = ctx.levels[-1]
+    x0, b = inputs(lev.level.total_dofs, np.float64)
+    outs = []
+    for _ in range(2):
+        xd = dev(cuda, x0.copy())
+        pmg.v_cycle(ctx, 2, xd, dev(cuda, b))
+        outs.append(xd.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
