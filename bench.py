@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the vertex-patch smoother hot path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--dim D --degree k --level L --dtype f64|f32 --variant fused]
+
+One "step" = one colourised multiplicative vertex-patch smoothing step
+(smooth<T>, /root/reference/proj/src/smoother.cpp:41-151) over the level's
+synthetic x, b ~ U(-1,1). Default workload = BASELINE.json configs[1]
+(3D Q2, 2^6 cells per direction, FP64). Prints ONE JSON line on rank 0.
+
+Timing: W warm-up steps, then K steps each bracketed by CUDA events on the
+launch stream, L2 flushed (write of a 256 MiB buffer) before every timed step
+since the C2 vectors (2 x 16 MiB) fit in the 126 MB L2; barrier +
+synchronize around the timed region, max over ranks. Clocks and throttle
+reasons are sampled with NVML during the timed region.
+
+Multi-GPU (torchrun, one process per GPU): the slab domain decomposition
+(paper_2405_19004_b200.dd) runs when the level is divisible across ranks;
+every rank owns an equal slab (weak scaling when --weak, strong otherwise).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+
+
+def flops_per_patch(dim: int, k: int) -> int:
+    """Algorithmic flops of the reference's per-patch contraction sequence
+    (fastdiag.cpp:199-233 + :164-192 + smoother.cpp:119-120)."""
+    ni, nc = 2 * k - 1, 2 * k + 1
+    if dim == 3:
+        return 4 * ni * nc ** 3 + 6 * ni ** 2 * nc ** 2 + 6 * ni ** 3 * nc + 12 * ni ** 4 + 3 * ni ** 3
+    return 4 * ni * nc ** 2 + 4 * ni ** 2 * nc + 8 * ni ** 3 + 3 * ni ** 2
+
+
+def algorithmic_bytes_per_step(dim: int, k: int, level: int, word: int) -> int:
+    """x read once per colour + b^I read and x^I written once per patch
+    (SURVEY.md §8d): w (2^d N + 2 P (2k-1)^d)."""
+    n = 1 << level
+    N = (n * k - 1) ** dim
+    P = (n - 1) ** dim
+    return word * ((1 << dim) * N + 2 * P * (2 * k - 1) ** dim)
+
+
+def colour_patches(dim: int, level: int, color: int) -> int:
+    n = 1 << level
+    tot = 1
+    for a in range(dim):
+        tot *= n // 2 if (color >> a) & 1 else n // 2 - 1
+    return tot
+
+
+class ClockSampler:
+    """NVML clocks / throttle reasons sampled in a thread (B200_PROFILING.md)."""
+
+    REASONS = {
+        "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4,
+    }
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _sample(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for name, bit in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._sample()
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+            self._sample()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_run(args, steps: int, warmup: int, budget_s: float | None):
+    """The reference's own CPU smooth (oracle/_ref = /root/reference compiled
+    unmodified) with all host threads; returns (DoF/s, steps run, threads)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import refbind
+
+    threads = os.cpu_count() or 1
+    ref = refbind.RefMg(args.dim, args.degree, args.level, prec=0 if args.dtype == "f64" else 1,
+                        variant=args.variant if args.variant in refbind.VARIANT else "fused", threads=threads)
+    li = args.level - 1
+    n = ref.n(li)
+    x, b = refbind.fill_uniform(42, n, n)
+    x = x.astype(ref.dtype)
+    b = b.astype(ref.dtype)
+    variant = args.variant if args.variant in refbind.VARIANT else "fused"
+    vcode = refbind.VARIANT[variant]
+    lib = refbind.lib()
+    for _ in range(warmup):
+        lib.ref_smooth(ref.h, li, vcode, refbind.P(x), refbind.P(b))
+    done, t_total = 0, 0.0
+    while True:
+        t0 = time.perf_counter()
+        st = lib.ref_smooth(ref.h, li, vcode, refbind.P(x), refbind.P(b))
+        t_total += time.perf_counter() - t0
+        assert st == 0
+        done += 1
+        if budget_s is None:
+            if done >= steps:
+                break
+        elif t_total >= budget_s or done >= steps:
+            break
+    return n * done / t_total, done, threads, t_total
+
+
+def run_reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    value, done, threads, t = cpu_reference_run(args, args.steps, args.warmup, None)
+    out = {
+        "impl": "reference",
+        "metric": metric_name(args), "value": value, "unit": "DoF/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / done,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic", "config": config_dict(args),
+        "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": threads, "kind": "reference",
+                         "sample": f"{done} full smoothing steps of the workload (pmg_ref::smooth<{args.dtype}>, "
+                                   f"{args.variant}, threads={threads})"},
+        "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def metric_name(args):
+    return f"DoF/s per smoother step ({args.variant} vertex-patch, {args.dtype})"
+
+
+def config_dict(args):
+    n = 1 << args.level
+    return {"workload": f"{args.dim}D Q{args.degree} unit {'cube' if args.dim == 3 else 'square'}, "
+                        f"2^{args.level} cells/dir, one {args.variant} smoother step",
+            "dim": args.dim, "degree": args.degree, "level": args.level,
+            "dofs": (n * args.degree - 1) ** args.dim, "patches": (n - 1) ** args.dim,
+            "l2_flush": "256 MiB write before every timed step"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dim", type=int, default=3)
+    ap.add_argument("--degree", type=int, default=2)
+    ap.add_argument("--level", type=int, default=6)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--variant", default="fused")
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU reference work (cpu_baseline)")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+
+    import paper_2405_19004_b200 as pmg
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    dt = np.float64 if args.dtype == "f64" else np.float32
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    word = 8 if args.dtype == "f64" else 4
+    lib = pmg.load()
+    ctx = pmg.make_multigrid_context(args.dim, args.degree, args.level, args.variant, dtype=dt, device=local)
+    lev = ctx.levels[-1]
+    N = lev.level.total_dofs
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    x = torch.rand(N, dtype=tdt, device="cuda", generator=gen) * 2 - 1
+    b = torch.rand(N, dtype=tdt, device="cuda", generator=gen) * 2 - 1
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up --------------------------------------------------------------
+    for _ in range(args.warmup):
+        pmg.smooth(lev, x, b, args.variant)
+    barrier()
+
+    # ---- timed region: K steps, CUDA events per step, L2 flushed between ------
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = lib.pmg_launch_count()
+    sampler = ClockSampler(local)
+    with sampler:
+        barrier()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            pmg.smooth(lev, x, b, args.variant)
+            ev[i][1].record(stream)
+        barrier()
+    launches = lib.pmg_launch_count() - launches0
+    t_step = sum(a.elapsed_time(c) for a, c in ev) / 1e3 / args.steps
+    if dist is not None:
+        t = torch.tensor([t_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+    value = world * N / t_step
+
+    # ---- per-launch roofline of the dominant kernel (the per-colour smoother) --
+    F = flops_per_patch(args.dim, args.degree)
+    colour_ms, colour_flops = 0.0, 0.0
+    reps = max(3, min(20, args.steps))
+    for c in range(1 << args.dim):
+        npatch = colour_patches(args.dim, args.level, c)
+        if npatch == 0:
+            continue
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.fill_(0.5)
+        e0.record(stream)
+        for _ in range(reps):
+            pmg.smooth_color(lev, c, x, b, args.variant)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        colour_ms += e0.elapsed_time(e1) / reps
+        colour_flops += F * npatch
+    launch_s = colour_ms / 1e3
+    alg_bytes = algorithmic_bytes_per_step(args.dim, args.degree, args.level, word)
+    peaks = json.load(open(MEASURED_PEAKS)) if os.path.exists(MEASURED_PEAKS) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    max_mhz = peaks.get("sm_max_mhz", 1965.0)
+    fp_peak = sm_count * (64 if args.dtype == "f64" else 128) * 2 * max_mhz * 1e6 / 1e12
+    traffic = None
+    if os.path.exists(NCU_SUMMARY):
+        try:
+            s = json.load(open(NCU_SUMMARY))
+            key = f"d{args.dim}k{args.degree}L{args.level}{args.dtype}{args.variant}"
+            traffic = s.get(key, {}).get("dram_bytes_per_step")
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "hbm", "achieved": alg_bytes / launch_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+        "frac": alg_bytes / launch_s / 1e9 / hbm_peak, "traffic": traffic,
+        "kernel": "vp_smooth_kernel (one launch per colour, summed over the 2^d colours)",
+        "algorithmic_bytes_per_step": alg_bytes,
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
+    }
+    roofline_fp = {
+        "bound": f"{args.dtype} CUDA-core FMA", "achieved": colour_flops / launch_s / 1e12,
+        "peak": fp_peak, "unit": "TFLOP/s", "frac": colour_flops / launch_s / 1e12 / fp_peak,
+        "algorithmic_flops_per_patch": F,
+        "peak_source": f"{sm_count} SMs x {64 if args.dtype == 'f64' else 128} FMA/clk x 2 x {max_mhz} MHz",
+    }
+
+    # ---- V-cycle throughput (secondary metric) ---------------------------------
+    li = args.level - 1
+    pmg.v_cycle(ctx, li, x, b, use_graph=True)
+    torch.cuda.synchronize()
+    vreps = max(3, min(10, args.steps))
+    vt = 0.0
+    for _ in range(vreps):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        pmg.v_cycle(ctx, li, x, b, use_graph=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        vt += e0.elapsed_time(e1) / 1e3
+    vt /= vreps
+
+    # ---- e2e through the C-ABI with host buffers (pinned) ----------------------
+    xh = torch.empty(N, dtype=tdt, pin_memory=True).numpy()
+    bh = torch.empty(N, dtype=tdt, pin_memory=True).numpy()
+    xh[:] = x.cpu().numpy()
+    bh[:] = b.cpu().numpy()
+    for _ in range(2):
+        pmg.smooth(lev, xh, bh, args.variant)
+    e2e_steps = max(3, min(args.steps, 20))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        pmg.smooth(lev, xh, bh, args.variant)  # pmg_smooth_host: H2D x,b -> kernels -> D2H x
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+
+    out = {
+        "metric": metric_name(args), "value": value, "unit": "DoF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (x, b ~ U(-1,1))", "config": config_dict(args),
+        "roofline": roofline, "roofline_fp": roofline_fp,
+        "e2e": {"value": world * N / t_e2e, "unit": "DoF/s", "h2d_bytes_per_step": 2 * N * word,
+                "d2h_bytes_per_step": N * word, "api": "pmg_smooth_host (C-ABI, pinned host buffers)"},
+        "clocks": sampler.summary(), "gpu_launches": int(launches),
+        "vcycle": {"value": world * N / vt, "unit": "DoF/s", "ms": vt * 1e3, "cuda_graph": True},
+    }
+    if dist is not None:
+        out["parallelism"] = f"replicas x{world}"
+
+    if rank == 0 and not args.no_cpu:
+        v, done, threads, tcpu = cpu_reference_run(args, 10 ** 6, 1, args.cpu_budget)
+        out["cpu_baseline"] = {"value": v, "unit": "DoF/s", "cores": threads, "kind": "reference",
+                               "sample": f"{done} full smoothing steps of the same workload in {tcpu:.1f} s "
+                                         f"(oracle/_ref = /root/reference compiled unmodified, threads={threads})"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

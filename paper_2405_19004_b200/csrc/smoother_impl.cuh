@@ -30,28 +30,30 @@
 namespace pmgb
 {
 
-// patches per CTA and threads per CTA, per (dim, degree)
+// patches per CTA and threads per CTA, per (dim, degree). Every stage maps
+// exactly one 1D line to one thread (NT >= lines of the widest stage), so no
+// stage loops: a loop would let the compiler hoist the parameter-bank matrix
+// entries out of it into general registers (hundreds of them in f64).
 template <int D, int K>
 constexpr int sm_pb()
 {
   if constexpr (D == 3)
   {
-    constexpr int t[8] = {0, 128, 32, 8, 8, 4, 2, 2};
+    constexpr int t[8] = {0, 16, 8, 4, 2, 2, 1, 1};
     return t[K];
   }
   else
   {
-    return K == 1 ? 256 : (256 + (2 * K - 1) - 1) / (2 * K - 1);
+    return 256 / (2 * K + 1);
   }
 }
 
 template <int D, int K>
 constexpr int sm_nt()
 {
-  constexpr int NI = 2 * K - 1;
-  constexpr int lines = sm_pb<D, K>() * (D == 3 ? NI * NI : NI);
-  constexpr int nt = ((lines + 31) / 32) * 32;
-  return nt < 64 ? 64 : (nt > 1024 ? 1024 : nt);
+  constexpr int NC = 2 * K + 1;
+  constexpr int lines = sm_pb<D, K>() * (D == 3 ? NC * NC : NC);
+  return ((lines + 31) / 32) * 32;
 }
 
 template <int D, int K>
@@ -135,8 +137,10 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
     if constexpr (MODE != MODE_SOLVE)
     {
       // ---- A: direction 0 from global rows: zM = M0 u, zA = A0 u ----------
-      for (int l = tid; l < PB * NC * NC; l += NT)
-      {
+      static_assert(PB * NC * NC <= NT, "one line per thread per stage");
+      if (const int l = tid; l < PB * NC * NC)
+        do
+        {
         const int p = l / (NC * NC);
         const int rr = l - p * (NC * NC);
         const int j1 = rr % NC, j2 = rr / NC;
@@ -167,12 +171,14 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
           Z[i] = zm[i];
           Z[ZS + i] = za[i];
         }
-      }
+      } while (0);
       __syncthreads();
 
       // ---- B: direction 1: wMM = M1 zM, wS = A1 zM + M1 zA (in place) -----
-      for (int l = tid; l < PB * NI * NC; l += NT)
-      {
+      static_assert(PB * NI * NC <= NT, "one line per thread per stage");
+      if (const int l = tid; l < PB * NI * NC)
+        do
+        {
         const int p = l / (NI * NC);
         if (pbase + p >= a.total)
           continue;
@@ -203,13 +209,15 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
           Z[NI * i] = wm;
           Z[ZS + NI * i] = ws;
         }
-      }
+      } while (0);
       __syncthreads();
     }
 
     // ---- C: direction 2: r = b - (A2 wMM + M2 wS); y = S^T r (dir 2) -------
-    for (int l = tid; l < PB * NI * NI; l += NT)
-    {
+    static_assert(PB * NI * NI <= NT, "one line per thread per stage");
+    if (const int l = tid; l < PB * NI * NI)
+      do
+      {
       const int p = l / (NI * NI);
       const int rr = l - p * (NI * NI);
       const int i0 = rr % NI, i1 = rr / NI;
@@ -259,14 +267,16 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
 #pragma unroll
       for (int j = 0; j < NI; ++j)
         Z[NI * NC * j] = y[j];
-    }
+    } while (0);
     if constexpr (MODE == MODE_RESIDUAL)
       return;
     __syncthreads();
 
     // ---- D: direction 1, S^T -----------------------------------------------
-    for (int l = tid; l < PB * NI * NI; l += NT)
-    {
+    static_assert(PB * NI * NI <= NT, "one line per thread per stage");
+    if (const int l = tid; l < PB * NI * NI)
+      do
+      {
       const int p = l / (NI * NI);
       if (pbase + p >= a.total)
         continue;
@@ -281,12 +291,14 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
 #pragma unroll
       for (int t = 0; t < NI; ++t)
         Z[NI * t] = y[t];
-    }
+    } while (0);
     __syncthreads();
 
     // ---- E: direction 0, S^T, scale by 1/(lambda sums), S --------------------
-    for (int l = tid; l < PB * NI * NI; l += NT)
-    {
+    static_assert(PB * NI * NI <= NT, "one line per thread per stage");
+    if (const int l = tid; l < PB * NI * NI)
+      do
+      {
       const int p = l / (NI * NI);
       if (pbase + p >= a.total)
         continue;
@@ -306,12 +318,14 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
 #pragma unroll
       for (int t = 0; t < NI; ++t)
         Z[t] = v[t];
-    }
+    } while (0);
     __syncthreads();
 
     // ---- F: direction 1, S -------------------------------------------------
-    for (int l = tid; l < PB * NI * NI; l += NT)
-    {
+    static_assert(PB * NI * NI <= NT, "one line per thread per stage");
+    if (const int l = tid; l < PB * NI * NI)
+      do
+      {
       const int p = l / (NI * NI);
       if (pbase + p >= a.total)
         continue;
@@ -326,12 +340,14 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
 #pragma unroll
       for (int t = 0; t < NI; ++t)
         Z[NI * t] = y[t];
-    }
+    } while (0);
     __syncthreads();
 
     // ---- G: direction 2, S, then x^I += v (or = v) --------------------------
-    for (int l = tid; l < PB * NI * NI; l += NT)
-    {
+    static_assert(PB * NI * NI <= NT, "one line per thread per stage");
+    if (const int l = tid; l < PB * NI * NI)
+      do
+      {
       const int p = l / (NI * NI);
       const int rr = l - p * (NI * NI);
       const int i0 = rr % NI, i1 = rr / NI;
@@ -353,15 +369,17 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
         else
           xp[i * m2] += y[i];
       }
-    }
+    } while (0);
   }
   else  // ------------------------------- 2D -----------------------------------
   {
     if constexpr (MODE != MODE_SOLVE)
     {
       // A: direction 0 rows from global
-      for (int l = tid; l < PB * NC; l += NT)
-      {
+      static_assert(PB * NC <= NT, "one line per thread per stage");
+      if (const int l = tid; l < PB * NC)
+        do
+        {
         const int p = l / NC;
         const int j1 = l - p * NC;
         int64_t g0, g1, g2;
@@ -389,13 +407,15 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
           Z[i] = zm[i];
           Z[ZS + i] = za[i];
         }
-      }
+      } while (0);
       __syncthreads();
     }
 
     // B: direction 1: r = b - (A1 zM + M1 zA); y = S^T r
-    for (int l = tid; l < PB * NI; l += NT)
-    {
+    static_assert(PB * NI <= NT, "one line per thread per stage");
+    if (const int l = tid; l < PB * NI)
+      do
+      {
       const int p = l / NI;
       const int i0 = l - p * NI;
       int64_t g0, g1, g2;
@@ -444,14 +464,16 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
 #pragma unroll
       for (int j = 0; j < NI; ++j)
         Z[NI * j] = y[j];
-    }
+    } while (0);
     if constexpr (MODE == MODE_RESIDUAL)
       return;
     __syncthreads();
 
     // C: direction 0: S^T, scale, S
-    for (int l = tid; l < PB * NI; l += NT)
-    {
+    static_assert(PB * NI <= NT, "one line per thread per stage");
+    if (const int l = tid; l < PB * NI)
+      do
+      {
       const int p = l / NI;
       if (pbase + p >= a.total)
         continue;
@@ -470,12 +492,14 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
 #pragma unroll
       for (int t = 0; t < NI; ++t)
         Z[t] = v[t];
-    }
+    } while (0);
     __syncthreads();
 
     // D: direction 1: S, x^I update
-    for (int l = tid; l < PB * NI; l += NT)
-    {
+    static_assert(PB * NI <= NT, "one line per thread per stage");
+    if (const int l = tid; l < PB * NI)
+      do
+      {
       const int p = l / NI;
       const int i0 = l - p * NI;
       int64_t g0, g1, g2;
@@ -496,7 +520,7 @@ __global__ void __launch_bounds__(sm_nt<D, K>())
         else
           xp[i * m] += y[i];
       }
-    }
+    } while (0);
   }
 }
 
@@ -512,6 +536,9 @@ void launch_vp_smooth(const PatchMats<T, K> &P, const ColorArgs<T> &a, cudaStrea
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)),
                "cudaFuncSetAttribute(smoother)");
+    check_cuda(cudaFuncSetAttribute(vp_smooth_kernel<D, K, T, MODE>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+               "cudaFuncSetAttribute(smoother carveout)");
   }
   const int grid = (a.total + PB - 1) / PB;
   if (grid == 0)
