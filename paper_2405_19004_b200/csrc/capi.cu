@@ -73,7 +73,8 @@ struct pmg_level_s
   int sm_count = 148;
   size_t tsize = 8;
   std::vector<unsigned char> patch_mats, band_mats, prol_mats;  // param blobs in T
-  DevBuf inv;             // inverse eigenvalue sums (T)
+  DevBuf inv;             // inverse eigenvalue sums (T), reference mode order
+  DevBuf inv_eo;          // same, even-first mode order of the fused kernel
   DevBuf resid;           // global residual (global / separate variants)
   DevBuf naive_mats;      // Mif | Aif | S (T) for the straightforward kernel
   DevBuf naive_scratch;
@@ -183,7 +184,12 @@ template <typename T>
 void level_init(pmg_level_s *l)
 {
   const auto &S = l->S;
-  l->patch_mats = blob<T>({&S.mass_if, &S.stiff_if, &S.S});
+  {
+    std::vector<T> v(S.eo_mats.begin(), S.eo_mats.end());
+    l->patch_mats.resize(v.size() * sizeof(T));
+    std::memcpy(l->patch_mats.data(), v.data(), l->patch_mats.size());
+  }
+  upload<T>(l->inv_eo, S.inv_sums_eo);
   l->band_mats = blob_vec<T>(S.band_mass, S.band_stiff);
   l->prol_mats = blob<T>({&S.prolongation});
   upload<T>(l->inv, S.inv_sums);
@@ -203,7 +209,7 @@ ColorArgs<T> color_args(const pmg_level_s *l, int color, T *x, const T *b)
   a.x = x;
   a.b = b;
   a.r = l->resid.as<T>();
-  a.inv = l->inv.as<T>();
+  a.inv = l->inv_eo.as<T>();
   a.m = l->S.m;
   const int n = l->S.n;
   a.total = 1;
@@ -235,22 +241,22 @@ void smooth_color_impl(pmg_level_s *l, int variant, int color, T *x, const T *b,
   switch (variant)
   {
     case PMG_FUSED:
-      kt.smooth(l->patch_mats.data(), a, MODE_FUSED, s);
+      kt.smooth(l->patch_mats.data(), a, MODE_FUSED, l->sm_count, s);
       break;
     case PMG_BOUNDARY:
-      kt.smooth(l->patch_mats.data(), a, MODE_BOUNDARY, s);
+      kt.smooth(l->patch_mats.data(), a, MODE_BOUNDARY, l->sm_count, s);
       break;
     case PMG_SEPARATE:
       l->resid.ensure(static_cast<size_t>(l->S.N) * sizeof(T));
       a.r = l->resid.as<T>();
-      kt.smooth(l->patch_mats.data(), a, MODE_RESIDUAL, s);
-      kt.smooth(l->patch_mats.data(), a, MODE_SOLVE, s);
+      kt.smooth(l->patch_mats.data(), a, MODE_RESIDUAL, l->sm_count, s);
+      kt.smooth(l->patch_mats.data(), a, MODE_SOLVE, l->sm_count, s);
       break;
     case PMG_GLOBAL:
       l->resid.ensure(static_cast<size_t>(l->S.N) * sizeof(T));
       a.r = l->resid.as<T>();
       kt.level_op(l->band_mats.data(), x, b, a.r, l->S.m, l->sm_count, s);
-      kt.smooth(l->patch_mats.data(), a, MODE_SOLVE, s);
+      kt.smooth(l->patch_mats.data(), a, MODE_SOLVE, l->sm_count, s);
       break;
     case PMG_NAIVE:
     {
@@ -259,6 +265,7 @@ void smooth_color_impl(pmg_level_s *l, int variant, int color, T *x, const T *b,
       l->naive_scratch.ensure(static_cast<size_t>(per) * grid * sizeof(T));
       NaiveArgs<T> na{};
       na.c = a;
+      na.c.inv = l->inv.as<T>();
       const int ni = 2 * l->S.k - 1, nc = 2 * l->S.k + 1;
       na.Mif = l->naive_mats.as<T>();
       na.Aif = na.Mif + ni * nc;

@@ -59,6 +59,26 @@ struct PatchMats
   T S[NI][NI];  // generalized eigenvectors, columns              (fastdiag.hpp:52)
 };
 
+// Even-odd form of PatchMats used by the fused kernel. The interior rows of
+// the two-cell matrices are centro-symmetric, B[NI-1-i][NC-1-j] = B[i][j]:
+//   Be[i][j] = (B[i][j] + B[i][NC-1-j]) / 2 (j < K), Be[i][K] = B[i][K]  (i <= K-1)
+//   Bo[i][j] = (B[i][j] - B[i][NC-1-j]) / 2                           (i <  K-1)
+// The eigenvectors of the reflection-symmetric patch pencil are even or odd;
+// columns are reordered even-first (K even, K-1 odd modes):
+//   Se[i][c] = S[i][perm[c]]     (i <= K-1, c <= K-1)
+//   So[i][c] = S[i][perm[K+c]]   (i <  K-1, c <  K-1)
+template <typename T, int K>
+struct PatchMatsEO
+{
+  static constexpr int HO = K > 1 ? K - 1 : 1;
+  T Me[K][K + 1];
+  T Mo[HO][K];
+  T Ae[K][K + 1];
+  T Ao[HO][K];
+  T Se[K][K];
+  T So[HO][HO];
+};
+
 // Rows of the global 1D matrices by lattice residue r = p mod K, offsets
 // o = q - p + K in [0, 2K]; the level operator is their Kronecker sum.
 template <typename T, int K>

@@ -10,8 +10,8 @@ namespace pmgb
 template <typename T>
 struct KernelTable
 {
-  // P: PatchMats<T,K>*; mode: MODE_*
-  void (*smooth)(const void *P, const ColorArgs<T> &a, int mode, cudaStream_t s) = nullptr;
+  // P: PatchMatsEO<T,K>*; mode: MODE_*
+  void (*smooth)(const void *P, const ColorArgs<T> &a, int mode, int sm_count, cudaStream_t s) = nullptr;
   // B: BandMats<T,K>*; b == nullptr -> y = A x, else y = b - A x
   void (*level_op)(const void *B, const T *x, const T *b, T *y, int64_t m, int sm_count,
                    cudaStream_t s) = nullptr;

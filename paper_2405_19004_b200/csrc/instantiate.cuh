@@ -16,9 +16,9 @@ namespace
 {
 
 template <int D, typename T>
-void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, cudaStream_t s)
+void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, cudaStream_t s)
 {
-  launch_vp_smooth_mode<D, PMG_K, T>(*static_cast<const PatchMats<T, PMG_K> *>(P), a, mode, s);
+  launch_vp_smooth_mode<D, PMG_K, T>(*static_cast<const PatchMatsEO<T, PMG_K> *>(P), a, mode, sm_count, s);
 }
 
 template <int D, typename T>
@@ -52,8 +52,8 @@ KernelTable<T> make_table()
   t.prolongate = &prol_entry<D, T>;
   t.restrict_ = &rest_entry<D, T>;
   t.smooth_smem = sm_smem_bytes<D, PMG_K, T>();
-  t.smooth_threads = sm_nt<D, PMG_K>();
-  t.smooth_pb = sm_pb<D, PMG_K>();
+  t.smooth_threads = sm_nt<D, PMG_K, T>();
+  t.smooth_pb = sm_pb<D, PMG_K, T>();
   return t;
 }
 

@@ -357,6 +357,65 @@ LevelSetup make_level_setup(int dim, int k, int level)
     s.inv_sums[idx] = 1.0 / sum;
   }
 
+  // even-odd data: the two-cell patch is reflection symmetric, so the
+  // interior-row matrices are centro-symmetric and every eigenvector is even
+  // or odd. Reorder the modes even-first (K even, K-1 odd), keep the
+  // ascending order inside each class.
+  {
+    const int K = k, HO = K > 1 ? K - 1 : 1;
+    std::vector<int> even, odd;
+    for (int j = 0; j < ni; ++j)
+    {
+      double de = 0, dodd = 0, nrm = 0;
+      for (int i = 0; i < ni; ++i)
+      {
+        de = std::max(de, std::fabs(s.S(ni - 1 - i, j) - s.S(i, j)));
+        dodd = std::max(dodd, std::fabs(s.S(ni - 1 - i, j) + s.S(i, j)));
+        nrm = std::max(nrm, std::fabs(s.S(i, j)));
+      }
+      if (de <= 1e-10 * nrm)
+        even.push_back(j);
+      else if (dodd <= 1e-10 * nrm)
+        odd.push_back(j);
+      else
+        throw std::runtime_error("patch eigenvector without reflection parity");
+    }
+    if (static_cast<int>(even.size()) != K || static_cast<int>(odd.size()) != K - 1)
+      throw std::runtime_error("unexpected even/odd eigenvector counts");
+    s.eo_perm = even;
+    s.eo_perm.insert(s.eo_perm.end(), odd.begin(), odd.end());
+    auto &o = s.eo_mats;
+    o.clear();
+    auto push_eo = [&](const Dense &B) {
+      for (int i = 0; i < K; ++i)
+        for (int j = 0; j <= K; ++j)
+          o.push_back(j < K ? 0.5 * (B(i, j) + B(i, nc - 1 - j)) : B(i, K));
+      for (int i = 0; i < HO; ++i)
+        for (int j = 0; j < K; ++j)
+          o.push_back(i < K - 1 ? 0.5 * (B(i, j) - B(i, nc - 1 - j)) : 0.0);
+    };
+    push_eo(s.mass_if);
+    push_eo(s.stiff_if);
+    for (int i = 0; i < K; ++i)
+      for (int c = 0; c < K; ++c)
+        o.push_back(s.S(i, s.eo_perm[c]));
+    for (int i = 0; i < HO; ++i)
+      for (int c = 0; c < HO; ++c)
+        o.push_back((i < K - 1 && c < K - 1) ? s.S(i, s.eo_perm[K + c]) : 0.0);
+    s.inv_sums_eo.resize(tot);
+    for (size_t idx = 0; idx < tot; ++idx)
+    {
+      size_t r = idx;
+      double sum = 0.0;
+      for (int a = 0; a < dim; ++a)
+      {
+        sum += s.lambda[s.eo_perm[r % ni]];
+        r /= ni;
+      }
+      s.inv_sums_eo[idx] = 1.0 / sum;
+    }
+  }
+
   // embedding of the coarse cell basis into the two fine cells
   s.prolongation = Dense(nc, k + 1);
   for (int f = 0; f < 2; ++f)

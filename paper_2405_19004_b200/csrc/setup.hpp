@@ -48,6 +48,11 @@ struct LevelSetup
   std::vector<double> lambda;   // 2k-1, ascending
   std::vector<double> inv_sums; // (2k-1)^dim, direction 0 fastest
   Dense prolongation;           // (2k+1) x (k+1)
+  // even-odd form for the fused kernel (layout of PatchMatsEO<double,k>):
+  // Me | Mo | Ae | Ao | Se | So, eigen-modes reordered even-first (eo_perm)
+  std::vector<double> eo_mats;
+  std::vector<int> eo_perm;        // reordered mode c -> original column
+  std::vector<double> inv_sums_eo; // inverse eigenvalue sums in reordered mode order
   // Banded rows of the global 1D matrices, indexed by lattice residue
   // r = p mod k and offset o = q - p + k in [0, 2k].
   std::vector<double> band_mass, band_stiff;  // k * (2k+1)

@@ -1,27 +1,32 @@
 // Fused per-colour vertex-patch smoother kernel for sm_100a.
 //
 // Replaces the per-patch body of the reference's smooth<T>
-// (/root/reference/proj/src/smoother.cpp:109-126, fused; :128-148 boundary;
-// :82-108 separate) and its callees gather/scatter_interior
+// (/root/reference/proj/src/smoother.cpp:109-126 fused, :128-148 boundary,
+// :82-108 separate, :63-81 global) and its callees gather/scatter_interior
 // (patches.cpp:51-121), apply_patch_operator (fastdiag.cpp:199-233) and
 // apply_patch_inverse (fastdiag.cpp:164-192).
 //
-// Design (see DESIGN.md §3):
-//  * one launch per colour; a CTA owns PB patches of that colour;
+// Design (DESIGN.md §3):
+//  * one launch per colour, persistent CTAs: a CTA loops over batches of PB
+//    patches of the colour; the closure (2k+1)^d of x and the interior
+//    (2k-1)^d of b of the NEXT batch are fetched with cp.async (coalesced,
+//    zero-filled outside the domain = the Dirichlet elimination of
+//    patches.cpp:72-79) while the current batch computes;
 //  * every sum-factorisation contraction is done by a thread that holds one
-//    full 1D line of the tensor in registers and produces the whole output
-//    line; the 1D matrices are compile-time-indexed kernel parameters, so the
-//    inner loops are pure DFMA/FFMA with uniform-register operands;
-//  * shared memory only transposes lines between directions. All stages
-//    work IN PLACE in one buffer per patch (2 (2k-1)(2k+1)^2 words in 3D):
-//    each thread reads its whole input line before writing its output line
-//    into a subset of the same positions, which no other thread touches in
-//    that stage. Strides (1, 2k-1, (2k-1)(2k+1)) are odd, so every stage is
-//    bank-conflict free for 4- and 8-byte words;
-//  * the first contraction (direction 0) reads closure rows straight from
-//    HBM/L2 (contiguous per thread), the residual stage reads b and the final
-//    stage updates x along direction 2 lines (contiguous across the warp);
-//  * 3D residual uses 7 contractions instead of the reference's 8 by
+//    full 1D line in registers and writes the whole output line. One line
+//    per thread per stage: no stage loops, so the compiler never hoists the
+//    parameter-bank matrices into general registers. The 1D matrices are
+//    compile-time-indexed __grid_constant__ kernel parameters, so the inner
+//    loops are DFMA/FFMA with uniform-register operands;
+//  * even-odd factorisation: the patch mass/stiffness rows are
+//    centro-symmetric and the eigenvectors have parity (columns reordered
+//    even-first on the host), so every 1D contraction runs on half-length
+//    even/odd vectors (~1/3 fewer multiply-adds than the dense form);
+//  * shared memory only transposes lines between directions; the work
+//    buffer is reused IN PLACE (each thread reads its whole input line before
+//    writing its output line into a subset of the same positions, which no
+//    other thread touches in that stage);
+//  * the 3D residual uses 7 contractions instead of the reference's 8 by
 //    summing the two mass-in-direction-2 terms before the last contraction.
 #pragma once
 
@@ -30,11 +35,12 @@
 namespace pmgb
 {
 
-// patches per CTA and threads per CTA, per (dim, degree). Every stage maps
-// exactly one 1D line to one thread (NT >= lines of the widest stage), so no
-// stage loops: a loop would let the compiler hoist the parameter-bank matrix
-// entries out of it into general registers (hundreds of them in f64).
-template <int D, int K>
+// ---------------------------------------------------------------------------
+// launch geometry
+// ---------------------------------------------------------------------------
+
+// patches per CTA; NT covers the widest stage with one line per thread
+template <int D, int K, typename T>
 constexpr int sm_pb()
 {
   if constexpr (D == 3)
@@ -48,522 +54,769 @@ constexpr int sm_pb()
   }
 }
 
-template <int D, int K>
+// minimum resident CTAs per SM requested from the register allocator
+template <int D, int K, typename T>
+constexpr int sm_minb()
+{
+  return (D == 3 && K >= 5) ? 2 : 1;
+}
+
+template <int D, int K, typename T>
 constexpr int sm_nt()
 {
   constexpr int NC = 2 * K + 1;
-  constexpr int lines = sm_pb<D, K>() * (D == 3 ? NC * NC : NC);
+  constexpr int lines = sm_pb<D, K, T>() * (D == 3 ? NC * NC : NC);
   return ((lines + 31) / 32) * 32;
 }
 
+constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+// shared memory per patch, in words: closure U | b interior Bs | work Z
 template <int D, int K>
-constexpr int sm_patch_stride()
+constexpr int sm_u_words()
+{
+  return ipow(2 * K + 1, D);
+}
+template <int D, int K>
+constexpr int sm_b_words()
+{
+  return ipow(2 * K - 1, D) + 1;  // +1: odd patch stride
+}
+template <int D, int K>
+constexpr int sm_z_words()
 {
   constexpr int NC = 2 * K + 1, NI = 2 * K - 1;
-  constexpr int ZS = (D == 3) ? NI * NC * NC : NI * NC;
-  return 2 * ZS + 1;  // odd: patches in one warp never alias banks
+  return 2 * ((D == 3) ? NI * NC * NC : NI * NC) + 1;
 }
 
 template <int D, int K, typename T>
 constexpr size_t sm_smem_bytes()
 {
-  return static_cast<size_t>(sm_pb<D, K>()) * sm_patch_stride<D, K>() * sizeof(T);
+  return static_cast<size_t>(sm_pb<D, K, T>()) *
+         (sm_u_words<D, K>() + sm_b_words<D, K>() + sm_z_words<D, K>()) * sizeof(T);
 }
 
-// y = Mat x   (Mat rows = outputs)
-template <int NO, int NN, typename T>
-__device__ __forceinline__ void mat_vec(const T (&Mt)[NO][NN], const T (&in)[NN], T (&out)[NO])
+// ---------------------------------------------------------------------------
+// cp.async (LDGSTS); src_size 0 zero-fills the destination
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T *smem, const T *gmem, bool valid)
 {
-#pragma unroll
-  for (int i = 0; i < NO; ++i)
-  {
-    T s = Mt[i][0] * in[0];
-#pragma unroll
-    for (int j = 1; j < NN; ++j)
-      s = fma(Mt[i][j], in[j], s);
-    out[i] = s;
-  }
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Read one entry of a __grid_constant__ parameter matrix. The volatile load
+// is issued at the point of use, so the compiler can neither hoist the
+// parameter bank out of the persistent batch loop nor CSE it into general
+// registers: every multiply-add takes its coefficient from a uniform register
+// loaded right before it (LDCU), costing no per-thread registers.
+__device__ __forceinline__ double pc(const double &r)
+{
+  double v;
+  asm volatile("{ .reg .u64 pa; cvta.to.param.u64 pa, %1; ld.param.f64 %0, [pa]; }" : "=d"(v) : "l"(&r));
+  return v;
+}
+__device__ __forceinline__ float pc(const float &r)
+{
+  float v;
+  asm volatile("{ .reg .u64 pa; cvta.to.param.u64 pa, %1; ld.param.f32 %0, [pa]; }" : "=f"(v) : "l"(&r));
+  return v;
 }
 
-// y = Mat^T x
+// ---------------------------------------------------------------------------
+// even-odd 1D contractions (matrices from PatchMatsEO, see common.cuh)
+// ---------------------------------------------------------------------------
+
+// split a length-N (odd) line into even / odd halves and its middle entry
 template <int N, typename T>
-__device__ __forceinline__ void mat_t_vec(const T (&Mt)[N][N], const T (&in)[N], T (&out)[N])
+__device__ __forceinline__ void eo_split(const T (&x)[N], T (&xe)[N / 2 + 1], T (&xo)[N / 2 > 0 ? N / 2 : 1])
 {
+  constexpr int H = N / 2;
 #pragma unroll
-  for (int j = 0; j < N; ++j)
+  for (int j = 0; j < H; ++j)
   {
-    T s = Mt[0][j] * in[0];
+    xe[j] = x[j] + x[N - 1 - j];
+    xo[j] = x[j] - x[N - 1 - j];
+  }
+  xe[H] = x[H];
+}
+
+// y (NI) = B x with B (NI x NC) centro-symmetric, given x split (xe: HC+1, xo: HC)
+template <int K, typename T, typename BE, typename BO>
+__device__ __forceinline__ void eo_rows(const BE &Be, const BO &Bo, const T (&xe)[K + 1], const T (&xo)[K],
+                                        T (&y)[2 * K - 1])
+{
+  constexpr int HI = K - 1, HC = K;
 #pragma unroll
-    for (int i = 1; i < N; ++i)
-      s = fma(Mt[i][j], in[i], s);
-    out[j] = s;
+  for (int i = 0; i <= HI; ++i)
+  {
+    T e = Be[i][HC] * xe[HC];
+#pragma unroll
+    for (int j = 0; j < HC; ++j)
+      e = fma(Be[i][j], xe[j], e);
+    if (i < HI)
+    {
+      T o = Bo[i][0] * xo[0];
+#pragma unroll
+      for (int j = 1; j < HC; ++j)
+        o = fma(Bo[i][j], xo[j], o);
+      y[i] = e + o;
+      y[2 * K - 2 - i] = e - o;
+    }
+    else
+    {
+      y[i] = e;
+    }
   }
 }
+
+// y = B1 x1 + B2 x2 (both centro-symmetric NI x NC), x1/x2 split
+template <int K, typename T, typename BE, typename BO>
+__device__ __forceinline__ void eo_rows2(const BE &B1e, const BO &B1o, const T (&x1e)[K + 1],
+                                         const T (&x1o)[K], const BE &B2e, const BO &B2o,
+                                         const T (&x2e)[K + 1], const T (&x2o)[K], T (&y)[2 * K - 1])
+{
+  constexpr int HI = K - 1, HC = K;
+#pragma unroll
+  for (int i = 0; i <= HI; ++i)
+  {
+    T e = B1e[i][HC] * x1e[HC];
+    e = fma(B2e[i][HC], x2e[HC], e);
+#pragma unroll
+    for (int j = 0; j < HC; ++j)
+    {
+      e = fma(B1e[i][j], x1e[j], e);
+      e = fma(B2e[i][j], x2e[j], e);
+    }
+    if (i < HI)
+    {
+      T o = B1o[i][0] * x1o[0];
+      o = fma(B2o[i][0], x2o[0], o);
+#pragma unroll
+      for (int j = 1; j < HC; ++j)
+      {
+        o = fma(B1o[i][j], x1o[j], o);
+        o = fma(B2o[i][j], x2o[j], o);
+      }
+      y[i] = e + o;
+      y[2 * K - 2 - i] = e - o;
+    }
+    else
+    {
+      y[i] = e;
+    }
+  }
+}
+
+// yhat = S^T r (eigen index: K even modes first, then K-1 odd modes)
+template <int K, typename T, typename SE, typename SO>
+__device__ __forceinline__ void eo_st(const SE &Se, const SO &So, const T (&r)[2 * K - 1], T (&yh)[2 * K - 1])
+{
+  constexpr int NI = 2 * K - 1, HI = K - 1;
+  T re[K], ro[K > 1 ? K - 1 : 1];
+#pragma unroll
+  for (int i = 0; i < HI; ++i)
+  {
+    re[i] = r[i] + r[NI - 1 - i];
+    ro[i] = r[i] - r[NI - 1 - i];
+  }
+  re[HI] = r[HI];
+#pragma unroll
+  for (int c = 0; c <= HI; ++c)
+  {
+    T s = Se[HI][c] * re[HI];
+#pragma unroll
+    for (int i = 0; i < HI; ++i)
+      s = fma(Se[i][c], re[i], s);
+    yh[c] = s;
+  }
+#pragma unroll
+  for (int c = 0; c < HI; ++c)
+  {
+    T s = So[0][c] * ro[0];
+#pragma unroll
+    for (int i = 1; i < HI; ++i)
+      s = fma(So[i][c], ro[i], s);
+    yh[HI + 1 + c] = s;
+  }
+}
+
+// x = S yhat (back to physical index)
+template <int K, typename T, typename SE, typename SO>
+__device__ __forceinline__ void eo_s(const SE &Se, const SO &So, const T (&yh)[2 * K - 1], T (&x)[2 * K - 1])
+{
+  constexpr int NI = 2 * K - 1, HI = K - 1;
+#pragma unroll
+  for (int i = 0; i <= HI; ++i)
+  {
+    T e = Se[i][0] * yh[0];
+#pragma unroll
+    for (int c = 1; c <= HI; ++c)
+      e = fma(Se[i][c], yh[c], e);
+    if (i < HI)
+    {
+      T o = So[i][0] * yh[HI + 1];
+#pragma unroll
+      for (int c = 1; c < HI; ++c)
+        o = fma(So[i][c], yh[HI + 1 + c], o);
+      x[i] = e + o;
+      x[NI - 1 - i] = e - o;
+    }
+    else
+    {
+      x[i] = e;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
 
 template <int D, int K, typename T, int MODE>
-__global__ void __launch_bounds__(sm_nt<D, K>())
-    vp_smooth_kernel(const __grid_constant__ PatchMats<T, K> P, const __grid_constant__ ColorArgs<T> a)
+__global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
+    vp_smooth_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ ColorArgs<T> a)
 {
   constexpr int NC = 2 * K + 1, NI = 2 * K - 1;
-  constexpr int PB = sm_pb<D, K>(), NT = sm_nt<D, K>();
-  constexpr int ZS = (D == 3) ? NI * NC * NC : NI * NC;
-  constexpr int PSTR = sm_patch_stride<D, K>();
+  constexpr int PB = sm_pb<D, K, T>();
+  constexpr int NT = sm_nt<D, K, T>();
+  constexpr int NCD = ipow(NC, D), NID = ipow(NI, D);
+  constexpr int UW = sm_u_words<D, K>(), BW = sm_b_words<D, K>(), ZW = sm_z_words<D, K>();
+  constexpr int ZS = (ZW - 1) / 2;  // one work array (zM / wMM / r); the second follows
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *sm = reinterpret_cast<T *>(smem_raw);
+  T *U = reinterpret_cast<T *>(smem_raw);  // [PB][UW]
+  T *Bs = U + PB * UW;                     // [PB][BW]
+  T *Z = Bs + PB * BW;                     // [PB][ZW]
 
   const int tid = threadIdx.x;
-  const int pbase = blockIdx.x * PB;
   const int64_t m = a.m;
+  const int nbatch = (a.total + PB - 1) / PB;
 
-  // dof index of closure-local t = 0 per direction (patches.cpp:71:
-  // g_a = k (v_a - 1) - 1 + t_a)
-  auto origin = [&](int p, int64_t &g0, int64_t &g1, int64_t &g2) -> bool {
-    const int gp = pbase + p;
-    if (gp >= a.total)
-      return false;
-    const int j0 = gp % a.np[0];
-    const int rest = gp / a.np[0];
-    const int j1 = rest % a.np[1];
-    const int j2 = rest / a.np[1];
-    g0 = static_cast<int64_t>(K) * (2 * j0 + a.vb[0] - 1) - 1;
-    g1 = static_cast<int64_t>(K) * (2 * j1 + a.vb[1] - 1) - 1;
-    g2 = (D == 3) ? static_cast<int64_t>(K) * (2 * j2 + a.vb[2] - 1) - 1 : 0;
-    return true;
+  // Per-batch patch origins (dof index of closure-local t = 0 per direction,
+  // patches.cpp:71: g_a = k (v_a - 1) - 1 + t_a), double-buffered: slot it&1
+  // holds the batch being computed, slot (it+1)&1 the one being prefetched.
+  __shared__ int org[2][PB][3];
+  auto set_origin = [&](int slot, int bt_) {
+    if (tid < PB)
+    {
+      const int gp = bt_ * PB + tid;
+      int g0 = -(1 << 30), g1 = -(1 << 30), g2 = -(1 << 30);  // invalid patch: all loads masked
+      if (gp < a.total)
+      {
+        const int j0 = gp % a.np[0];
+        const int rest = gp / a.np[0];
+        const int j1 = rest % a.np[1];
+        const int j2 = rest / a.np[1];
+        g0 = K * (2 * j0 + a.vb[0] - 1) - 1;
+        g1 = K * (2 * j1 + a.vb[1] - 1) - 1;
+        g2 = (D == 3) ? K * (2 * j2 + a.vb[2] - 1) - 1 : 0;
+      }
+      org[slot][tid][0] = g0;
+      org[slot][tid][1] = g1;
+      org[slot][tid][2] = g2;
+    }
   };
 
-  if constexpr (D == 3)
-  {
-    const int64_t m2 = m * m;
-    if constexpr (MODE != MODE_SOLVE)
+  // prefetch the closure of the batch whose origins are in `slot` into U
+  // (coalesced, zero-filled outside the domain)
+  auto load_closure = [&](int slot) {
+#pragma unroll 1
+    for (int e = tid; e < PB * NCD; e += NT)
     {
-      // ---- A: direction 0 from global rows: zM = M0 u, zA = A0 u ----------
-      static_assert(PB * NC * NC <= NT, "one line per thread per stage");
-      if (const int l = tid; l < PB * NC * NC)
-        do
-        {
-        const int p = l / (NC * NC);
-        const int rr = l - p * (NC * NC);
-        const int j1 = rr % NC, j2 = rr / NC;
-        int64_t g0, g1, g2;
-        if (!origin(p, g0, g1, g2))
-          continue;
-        const int64_t y1 = g1 + j1, y2 = g2 + j2;
-        const bool rowok = static_cast<uint64_t>(y1) < static_cast<uint64_t>(m) &&
-                           static_cast<uint64_t>(y2) < static_cast<uint64_t>(m);
-        const bool shell_only = (MODE == MODE_BOUNDARY) && j1 >= 1 && j1 <= NC - 2 && j2 >= 1 &&
-                                j2 <= NC - 2;
-        const T *row = a.x + (y2 * m + y1) * m + g0;
-        T u[NC];
-#pragma unroll
-        for (int t = 0; t < NC; ++t)
-        {
-          const bool ok = rowok && static_cast<uint64_t>(g0 + t) < static_cast<uint64_t>(m) &&
-                          (!shell_only || t == 0 || t == NC - 1);
-          u[t] = ok ? __ldg(row + t) : T(0);
-        }
-        T zm[NI], za[NI];
-        mat_vec(P.M, u, zm);
-        mat_vec(P.A, u, za);
-        T *Z = sm + p * PSTR + NI * j1 + NI * NC * j2;
-#pragma unroll
-        for (int i = 0; i < NI; ++i)
-        {
-          Z[i] = zm[i];
-          Z[ZS + i] = za[i];
-        }
-      } while (0);
-      __syncthreads();
+      const int p = e / NCD, r = e - (e / NCD) * NCD;
+      const int t0 = r % NC, t1 = (r / NC) % NC, t2 = (D == 3) ? r / (NC * NC) : 0;
+      const int y0 = org[slot][p][0] + t0, y1 = org[slot][p][1] + t1, y2 = org[slot][p][2] + t2;
+      bool ok = static_cast<uint32_t>(y0) < static_cast<uint32_t>(m) &&
+                static_cast<uint32_t>(y1) < static_cast<uint32_t>(m) &&
+                (D == 2 || static_cast<uint32_t>(y2) < static_cast<uint32_t>(m));
+      if constexpr (MODE == MODE_BOUNDARY)
+      {
+        // boundary variant never reads x^I (smoother.cpp:128-148)
+        const bool inner = t0 >= 1 && t0 <= NC - 2 && t1 >= 1 && t1 <= NC - 2 &&
+                           (D == 2 || (t2 >= 1 && t2 <= NC - 2));
+        ok = ok && !inner;
+      }
+      const int64_t gi = (D == 3) ? (static_cast<int64_t>(y2) * m + y1) * m + y0 : static_cast<int64_t>(y1) * m + y0;
+      cp_async_elem(U + p * UW + r, ok ? a.x + gi : a.x, ok);
+    }
+  };
+  // prefetch the interior of b (or of the residual for MODE_SOLVE)
+  auto load_interior = [&](int slot) {
+    const T *vec = (MODE == MODE_SOLVE) ? a.r : a.b;
+#pragma unroll 1
+    for (int e = tid; e < PB * NID; e += NT)
+    {
+      const int p = e / NID, r = e - (e / NID) * NID;
+      const int i0 = r % NI, i1 = (r / NI) % NI, i2 = (D == 3) ? r / (NI * NI) : 0;
+      const int g0 = org[slot][p][0];
+      const bool ok = g0 > -(1 << 29);
+      const int64_t y0 = g0 + 1 + i0, y1 = org[slot][p][1] + 1 + i1, y2 = org[slot][p][2] + 1 + i2;
+      const int64_t gi = (D == 3) ? (y2 * m + y1) * m + y0 : y1 * m + y0;
+      cp_async_elem(Bs + p * BW + r, ok ? vec + gi : a.x, ok);
+    }
+  };
+  auto origin = [&](int slot, int p, int64_t &g0, int64_t &g1, int64_t &g2) {
+    g0 = org[slot][p][0];
+    g1 = org[slot][p][1];
+    g2 = org[slot][p][2];
+  };
 
-      // ---- B: direction 1: wMM = M1 zM, wS = A1 zM + M1 zA (in place) -----
-      static_assert(PB * NI * NC <= NT, "one line per thread per stage");
-      if (const int l = tid; l < PB * NI * NC)
-        do
+  // one batch of PB patches per CTA. (A persistent CTA looping over batches
+  // with a cp.async prefetch of the next batch was measured slower: the loop
+  // lets the compiler hoist the parameter-bank matrices into registers.)
+  const int bt = blockIdx.x;
+  if (bt >= nbatch)
+    return;
+  constexpr int cur = 0;
+  const int nxt = nbatch;  // no next batch to prefetch
+  set_origin(0, bt);
+  __syncthreads();
+  if constexpr (MODE != MODE_SOLVE)
+    load_closure(0);
+  load_interior(0);
+  cp_async_commit();
+  {
+    cp_async_wait_all();
+    __syncthreads();
+
+    if constexpr (D == 3)
+    {
+      const int64_t m2 = m * m;
+      if constexpr (MODE != MODE_SOLVE)
+      {
+        // ---- A: direction 0: zM = M0 u, zA = A0 u -----------------------------
+        static_assert(PB * NC * NC <= NT, "one line per thread per stage");
+        if (tid < PB * NC * NC)
         {
-        const int p = l / (NI * NC);
-        if (pbase + p >= a.total)
-          continue;
-        const int rr = l - p * (NI * NC);
-        const int i0 = rr % NI, j2 = rr / NI;
-        T *Z = sm + p * PSTR + i0 + NI * NC * j2;
-        T zm[NC], za[NC];
+          const int p = tid / (NC * NC);
+          const int rr = tid - p * (NC * NC);  // = j1 + NC j2
+          const T *u_ = U + p * UW + NC * rr;
+          T u[NC];
 #pragma unroll
-        for (int t = 0; t < NC; ++t)
-        {
-          zm[t] = Z[NI * t];
-          za[t] = Z[ZS + NI * t];
-        }
+          for (int t = 0; t < NC; ++t)
+            u[t] = u_[t];
+          T ue[K + 1], uo[K];
+          eo_split<NC>(u, ue, uo);
+          T zm[NI], za[NI];
+          eo_rows<K>(P.Me, P.Mo, ue, uo, zm);
+          eo_rows<K>(P.Ae, P.Ao, ue, uo, za);
+          T *z = Z + p * ZW + NI * rr;  // strides (1, NI, NI*NC)
 #pragma unroll
-        for (int i = 0; i < NI; ++i)
-        {
-          T wm = P.M[i][0] * zm[0];
-          T ws = P.A[i][0] * zm[0];
-#pragma unroll
-          for (int t = 1; t < NC; ++t)
+          for (int i = 0; i < NI; ++i)
           {
-            wm = fma(P.M[i][t], zm[t], wm);
-            ws = fma(P.A[i][t], zm[t], ws);
+            z[i] = zm[i];
+            z[ZS + i] = za[i];
           }
-#pragma unroll
-          for (int t = 0; t < NC; ++t)
-            ws = fma(P.M[i][t], za[t], ws);
-          Z[NI * i] = wm;
-          Z[ZS + NI * i] = ws;
         }
-      } while (0);
-      __syncthreads();
-    }
+        __syncthreads();
+        if (nxt < nbatch)
+        {
+          load_closure(cur ^ 1);  // U is free: overlap the next closure with B..G
+          cp_async_commit();
+        }
 
-    // ---- C: direction 2: r = b - (A2 wMM + M2 wS); y = S^T r (dir 2) -------
-    static_assert(PB * NI * NI <= NT, "one line per thread per stage");
-    if (const int l = tid; l < PB * NI * NI)
-      do
-      {
-      const int p = l / (NI * NI);
-      const int rr = l - p * (NI * NI);
-      const int i0 = rr % NI, i1 = rr / NI;
-      int64_t g0, g1, g2;
-      if (!origin(p, g0, g1, g2))
-        continue;
-      T *Z = sm + p * PSTR + i0 + NI * i1;
-      const int64_t gidx = ((g2 + 1) * m + (g1 + 1 + i1)) * m + (g0 + 1 + i0);
-      T r[NI];
-      if constexpr (MODE == MODE_SOLVE)
-      {
-#pragma unroll
-        for (int i = 0; i < NI; ++i)
-          r[i] = a.r[gidx + i * m2];
-      }
-      else
-      {
-        T wm[NC], ws[NC];
-#pragma unroll
-        for (int t = 0; t < NC; ++t)
+        // ---- B: direction 1: wMM = M1 zM, wS = A1 zM + M1 zA (in place) ------
+        if (tid < PB * NI * NC)
         {
-          wm[t] = Z[NI * NC * t];
-          ws[t] = Z[ZS + NI * NC * t];
-        }
-#pragma unroll
-        for (int i = 0; i < NI; ++i)
-        {
-          T acc = P.A[i][0] * wm[0];
-#pragma unroll
-          for (int t = 1; t < NC; ++t)
-            acc = fma(P.A[i][t], wm[t], acc);
+          const int p = tid / (NI * NC);
+          const int rr = tid - p * (NI * NC);
+          const int i0 = rr % NI, j2 = rr / NI;
+          T *z = Z + p * ZW + i0 + NI * NC * j2;
+          T zm[NC], za[NC];
 #pragma unroll
           for (int t = 0; t < NC; ++t)
-            acc = fma(P.M[i][t], ws[t], acc);
-          r[i] = __ldg(a.b + gidx + i * m2) - acc;
-        }
-        if constexpr (MODE == MODE_RESIDUAL)
-        {
+          {
+            zm[t] = z[NI * t];
+            za[t] = z[ZS + NI * t];
+          }
+          T zme[K + 1], zmo[K], zae[K + 1], zao[K];
+          eo_split<NC>(zm, zme, zmo);
+          eo_split<NC>(za, zae, zao);
+          T wm[NI], ws[NI];
+          eo_rows<K>(P.Me, P.Mo, zme, zmo, wm);
+          eo_rows2<K>(P.Ae, P.Ao, zme, zmo, P.Me, P.Mo, zae, zao, ws);
 #pragma unroll
           for (int i = 0; i < NI; ++i)
-            a.r[gidx + i * m2] = r[i];
-          continue;
+          {
+            z[NI * i] = wm[i];
+            z[ZS + NI * i] = ws[i];
+          }
+        }
+        __syncthreads();
+      }
+
+      // ---- C: direction 2: r = b - (A2 wMM + M2 wS); yhat = S^T r ------------
+      if (tid < PB * NI * NI)
+      {
+        const int p = tid / (NI * NI);
+        const int rr = tid - p * (NI * NI);  // = i0 + NI i1
+        const int i0 = rr % NI, i1 = rr / NI;
+        const int gp = bt * PB + p;
+        if (gp < a.total)
+        {
+          T *z = Z + p * ZW + rr;
+          const T *bl = Bs + p * BW + rr;
+          T r[NI];
+          if constexpr (MODE == MODE_SOLVE)
+          {
+#pragma unroll
+            for (int i = 0; i < NI; ++i)
+              r[i] = bl[NI * NI * i];
+          }
+          else
+          {
+            T wm[NC], ws[NC];
+#pragma unroll
+            for (int t = 0; t < NC; ++t)
+            {
+              wm[t] = z[NI * NC * t];
+              ws[t] = z[ZS + NI * NC * t];
+            }
+            T wme[K + 1], wmo[K], wse[K + 1], wso[K];
+            eo_split<NC>(wm, wme, wmo);
+            eo_split<NC>(ws, wse, wso);
+            T acc[NI];
+            eo_rows2<K>(P.Ae, P.Ao, wme, wmo, P.Me, P.Mo, wse, wso, acc);
+#pragma unroll
+            for (int i = 0; i < NI; ++i)
+              r[i] = bl[NI * NI * i] - acc[i];
+            if constexpr (MODE == MODE_RESIDUAL)
+            {
+              int64_t g0, g1, g2;
+              origin(cur, p, g0, g1, g2);
+              T *rp = a.r + ((g2 + 1) * m + (g1 + 1 + i1)) * m + (g0 + 1 + i0);
+#pragma unroll
+              for (int i = 0; i < NI; ++i)
+                rp[i * m2] = r[i];
+            }
+          }
+          if constexpr (MODE != MODE_RESIDUAL)
+          {
+            T y[NI];
+            eo_st<K>(P.Se, P.So, r, y);
+#pragma unroll
+            for (int c = 0; c < NI; ++c)
+              z[NI * NC * c] = y[c];
+          }
         }
       }
-      T y[NI];
-      mat_t_vec(P.S, r, y);
-#pragma unroll
-      for (int j = 0; j < NI; ++j)
-        Z[NI * NC * j] = y[j];
-    } while (0);
-    if constexpr (MODE == MODE_RESIDUAL)
-      return;
-    __syncthreads();
-
-    // ---- D: direction 1, S^T -----------------------------------------------
-    static_assert(PB * NI * NI <= NT, "one line per thread per stage");
-    if (const int l = tid; l < PB * NI * NI)
-      do
+      if constexpr (MODE == MODE_RESIDUAL)
       {
-      const int p = l / (NI * NI);
-      if (pbase + p >= a.total)
-        continue;
-      const int rr = l - p * (NI * NI);
-      const int i0 = rr % NI, i2 = rr / NI;
-      T *Z = sm + p * PSTR + i0 + NI * NC * i2;
-      T v[NI], y[NI];
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-        v[t] = Z[NI * t];
-      mat_t_vec(P.S, v, y);
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-        Z[NI * t] = y[t];
-    } while (0);
-    __syncthreads();
-
-    // ---- E: direction 0, S^T, scale by 1/(lambda sums), S --------------------
-    static_assert(PB * NI * NI <= NT, "one line per thread per stage");
-    if (const int l = tid; l < PB * NI * NI)
-      do
-      {
-      const int p = l / (NI * NI);
-      if (pbase + p >= a.total)
-        continue;
-      const int rr = l - p * (NI * NI);
-      const int i1 = rr % NI, i2 = rr / NI;
-      T *Z = sm + p * PSTR + NI * i1 + NI * NC * i2;
-      const T *inv = a.inv + NI * i1 + NI * NI * i2;
-      T v[NI], y[NI];
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-        v[t] = Z[t];
-      mat_t_vec(P.S, v, y);
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-        y[t] *= __ldg(inv + t);
-      mat_vec(P.S, y, v);
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-        Z[t] = v[t];
-    } while (0);
-    __syncthreads();
-
-    // ---- F: direction 1, S -------------------------------------------------
-    static_assert(PB * NI * NI <= NT, "one line per thread per stage");
-    if (const int l = tid; l < PB * NI * NI)
-      do
-      {
-      const int p = l / (NI * NI);
-      if (pbase + p >= a.total)
-        continue;
-      const int rr = l - p * (NI * NI);
-      const int i0 = rr % NI, i2 = rr / NI;
-      T *Z = sm + p * PSTR + i0 + NI * NC * i2;
-      T v[NI], y[NI];
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-        v[t] = Z[NI * t];
-      mat_vec(P.S, v, y);
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-        Z[NI * t] = y[t];
-    } while (0);
-    __syncthreads();
-
-    // ---- G: direction 2, S, then x^I += v (or = v) --------------------------
-    static_assert(PB * NI * NI <= NT, "one line per thread per stage");
-    if (const int l = tid; l < PB * NI * NI)
-      do
-      {
-      const int p = l / (NI * NI);
-      const int rr = l - p * (NI * NI);
-      const int i0 = rr % NI, i1 = rr / NI;
-      int64_t g0, g1, g2;
-      if (!origin(p, g0, g1, g2))
-        continue;
-      const T *Z = sm + p * PSTR + i0 + NI * i1;
-      T v[NI], y[NI];
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-        v[t] = Z[NI * NC * t];
-      mat_vec(P.S, v, y);
-      T *xp = a.x + ((g2 + 1) * m + (g1 + 1 + i1)) * m + (g0 + 1 + i0);
-#pragma unroll
-      for (int i = 0; i < NI; ++i)
-      {
-        if constexpr (MODE == MODE_BOUNDARY)
-          xp[i * m2] = y[i];
-        else
-          xp[i * m2] += y[i];
+        __syncthreads();
+        if (nxt < nbatch)
+        {
+          load_interior(cur ^ 1);
+          cp_async_commit();
+        }
+        return;
       }
-    } while (0);
-  }
-  else  // ------------------------------- 2D -----------------------------------
-  {
-    if constexpr (MODE != MODE_SOLVE)
+      __syncthreads();
+      if (nxt < nbatch)
+      {
+        load_interior(cur ^ 1);  // Bs is free: overlap the next b with D..G
+        cp_async_commit();
+      }
+
+      // ---- D: direction 1, S^T ---------------------------------------------------
+      if (tid < PB * NI * NI)
+      {
+        const int p = tid / (NI * NI);
+        const int rr = tid - p * (NI * NI);
+        const int i0 = rr % NI, i2 = rr / NI;
+        T *z = Z + p * ZW + i0 + NI * NC * i2;
+        T v[NI], y[NI];
+#pragma unroll
+        for (int t = 0; t < NI; ++t)
+          v[t] = z[NI * t];
+        eo_st<K>(P.Se, P.So, v, y);
+#pragma unroll
+        for (int t = 0; t < NI; ++t)
+          z[NI * t] = y[t];
+      }
+      __syncthreads();
+
+      // ---- E: direction 0, S^T, scale by 1/(lambda sums), S -----------------------
+      if (tid < PB * NI * NI)
+      {
+        const int p = tid / (NI * NI);
+        const int rr = tid - p * (NI * NI);
+        const int i1 = rr % NI, i2 = rr / NI;
+        T *z = Z + p * ZW + NI * i1 + NI * NC * i2;
+        const T *inv = a.inv + NI * rr;
+        T v[NI], y[NI];
+#pragma unroll
+        for (int t = 0; t < NI; ++t)
+          v[t] = z[t];
+        eo_st<K>(P.Se, P.So, v, y);
+#pragma unroll
+        for (int t = 0; t < NI; ++t)
+          y[t] *= __ldg(inv + t);
+        eo_s<K>(P.Se, P.So, y, v);
+#pragma unroll
+        for (int t = 0; t < NI; ++t)
+          z[t] = v[t];
+      }
+      __syncthreads();
+
+      // ---- F: direction 1, S -------------------------------------------------------
+      if (tid < PB * NI * NI)
+      {
+        const int p = tid / (NI * NI);
+        const int rr = tid - p * (NI * NI);
+        const int i0 = rr % NI, i2 = rr / NI;
+        T *z = Z + p * ZW + i0 + NI * NC * i2;
+        T v[NI], y[NI];
+#pragma unroll
+        for (int t = 0; t < NI; ++t)
+          v[t] = z[NI * t];
+        eo_s<K>(P.Se, P.So, v, y);
+#pragma unroll
+        for (int t = 0; t < NI; ++t)
+          z[NI * t] = y[t];
+      }
+      __syncthreads();
+
+      // ---- G: direction 2, S, then x^I += v (or = v) -------------------------------
+      if (tid < PB * NI * NI)
+      {
+        const int p = tid / (NI * NI);
+        const int rr = tid - p * (NI * NI);
+        const int i0 = rr % NI, i1 = rr / NI;
+        const int gp = bt * PB + p;
+        if (gp < a.total)
+        {
+          int64_t g0, g1, g2;
+          origin(cur, p, g0, g1, g2);
+          const T *z = Z + p * ZW + rr;
+          T v[NI], y[NI];
+#pragma unroll
+          for (int t = 0; t < NI; ++t)
+            v[t] = z[NI * NC * t];
+          eo_s<K>(P.Se, P.So, v, y);
+          T *xp = a.x + ((g2 + 1) * m + (g1 + 1 + i1)) * m + (g0 + 1 + i0);
+#pragma unroll
+          for (int i = 0; i < NI; ++i)
+          {
+            if constexpr (MODE == MODE_BOUNDARY)
+              xp[i * m2] = y[i];
+            else
+              xp[i * m2] += y[i];
+          }
+        }
+      }
+    }
+    else  // ------------------------------- 2D -----------------------------------------
     {
-      // A: direction 0 rows from global
-      static_assert(PB * NC <= NT, "one line per thread per stage");
-      if (const int l = tid; l < PB * NC)
-        do
-        {
-        const int p = l / NC;
-        const int j1 = l - p * NC;
-        int64_t g0, g1, g2;
-        if (!origin(p, g0, g1, g2))
-          continue;
-        const int64_t y1 = g1 + j1;
-        const bool rowok = static_cast<uint64_t>(y1) < static_cast<uint64_t>(m);
-        const bool shell_only = (MODE == MODE_BOUNDARY) && j1 >= 1 && j1 <= NC - 2;
-        const T *row = a.x + y1 * m + g0;
-        T u[NC];
-#pragma unroll
-        for (int t = 0; t < NC; ++t)
-        {
-          const bool ok = rowok && static_cast<uint64_t>(g0 + t) < static_cast<uint64_t>(m) &&
-                          (!shell_only || t == 0 || t == NC - 1);
-          u[t] = ok ? __ldg(row + t) : T(0);
-        }
-        T zm[NI], za[NI];
-        mat_vec(P.M, u, zm);
-        mat_vec(P.A, u, za);
-        T *Z = sm + p * PSTR + NI * j1;
-#pragma unroll
-        for (int i = 0; i < NI; ++i)
-        {
-          Z[i] = zm[i];
-          Z[ZS + i] = za[i];
-        }
-      } while (0);
-      __syncthreads();
-    }
-
-    // B: direction 1: r = b - (A1 zM + M1 zA); y = S^T r
-    static_assert(PB * NI <= NT, "one line per thread per stage");
-    if (const int l = tid; l < PB * NI)
-      do
+      if constexpr (MODE != MODE_SOLVE)
       {
-      const int p = l / NI;
-      const int i0 = l - p * NI;
-      int64_t g0, g1, g2;
-      if (!origin(p, g0, g1, g2))
-        continue;
-      T *Z = sm + p * PSTR + i0;
-      const int64_t gidx = (g1 + 1) * m + (g0 + 1 + i0);
-      T r[NI];
-      if constexpr (MODE == MODE_SOLVE)
-      {
-#pragma unroll
-        for (int i = 0; i < NI; ++i)
-          r[i] = a.r[gidx + i * m];
-      }
-      else
-      {
-        T zm[NC], za[NC];
-#pragma unroll
-        for (int t = 0; t < NC; ++t)
+        // A: direction 0 rows: zM = M0 u, zA = A0 u
+        static_assert(PB * NC <= NT, "one line per thread per stage");
+        if (tid < PB * NC)
         {
-          zm[t] = Z[NI * t];
-          za[t] = Z[ZS + NI * t];
-        }
-#pragma unroll
-        for (int i = 0; i < NI; ++i)
-        {
-          T acc = P.A[i][0] * zm[0];
-#pragma unroll
-          for (int t = 1; t < NC; ++t)
-            acc = fma(P.A[i][t], zm[t], acc);
+          const int p = tid / NC;
+          const int j1 = tid - p * NC;
+          const T *u_ = U + p * UW + NC * j1;
+          T u[NC];
 #pragma unroll
           for (int t = 0; t < NC; ++t)
-            acc = fma(P.M[i][t], za[t], acc);
-          r[i] = __ldg(a.b + gidx + i * m) - acc;
-        }
-        if constexpr (MODE == MODE_RESIDUAL)
-        {
+            u[t] = u_[t];
+          T ue[K + 1], uo[K];
+          eo_split<NC>(u, ue, uo);
+          T zm[NI], za[NI];
+          eo_rows<K>(P.Me, P.Mo, ue, uo, zm);
+          eo_rows<K>(P.Ae, P.Ao, ue, uo, za);
+          T *z = Z + p * ZW + NI * j1;
 #pragma unroll
           for (int i = 0; i < NI; ++i)
-            a.r[gidx + i * m] = r[i];
-          continue;
+          {
+            z[i] = zm[i];
+            z[ZS + i] = za[i];
+          }
+        }
+        __syncthreads();
+        if (nxt < nbatch)
+        {
+          load_closure(cur ^ 1);
+          cp_async_commit();
         }
       }
-      T y[NI];
-      mat_t_vec(P.S, r, y);
-#pragma unroll
-      for (int j = 0; j < NI; ++j)
-        Z[NI * j] = y[j];
-    } while (0);
-    if constexpr (MODE == MODE_RESIDUAL)
-      return;
-    __syncthreads();
 
-    // C: direction 0: S^T, scale, S
-    static_assert(PB * NI <= NT, "one line per thread per stage");
-    if (const int l = tid; l < PB * NI)
-      do
+      // B: direction 1: r = b - (A1 zM + M1 zA); yhat = S^T r
+      if (tid < PB * NI)
       {
-      const int p = l / NI;
-      if (pbase + p >= a.total)
-        continue;
-      const int i1 = l - p * NI;
-      T *Z = sm + p * PSTR + NI * i1;
-      const T *inv = a.inv + NI * i1;
-      T v[NI], y[NI];
+        const int p = tid / NI;
+        const int i0 = tid - p * NI;
+        const int gp = bt * PB + p;
+        if (gp < a.total)
+        {
+          T *z = Z + p * ZW + i0;
+          const T *bl = Bs + p * BW + i0;
+          T r[NI];
+          if constexpr (MODE == MODE_SOLVE)
+          {
 #pragma unroll
-      for (int t = 0; t < NI; ++t)
-        v[t] = Z[t];
-      mat_t_vec(P.S, v, y);
+            for (int i = 0; i < NI; ++i)
+              r[i] = bl[NI * i];
+          }
+          else
+          {
+            T zm[NC], za[NC];
 #pragma unroll
-      for (int t = 0; t < NI; ++t)
-        y[t] *= __ldg(inv + t);
-      mat_vec(P.S, y, v);
+            for (int t = 0; t < NC; ++t)
+            {
+              zm[t] = z[NI * t];
+              za[t] = z[ZS + NI * t];
+            }
+            T zme[K + 1], zmo[K], zae[K + 1], zao[K];
+            eo_split<NC>(zm, zme, zmo);
+            eo_split<NC>(za, zae, zao);
+            T acc[NI];
+            eo_rows2<K>(P.Ae, P.Ao, zme, zmo, P.Me, P.Mo, zae, zao, acc);
 #pragma unroll
-      for (int t = 0; t < NI; ++t)
-        Z[t] = v[t];
-    } while (0);
-    __syncthreads();
-
-    // D: direction 1: S, x^I update
-    static_assert(PB * NI <= NT, "one line per thread per stage");
-    if (const int l = tid; l < PB * NI)
-      do
-      {
-      const int p = l / NI;
-      const int i0 = l - p * NI;
-      int64_t g0, g1, g2;
-      if (!origin(p, g0, g1, g2))
-        continue;
-      const T *Z = sm + p * PSTR + i0;
-      T v[NI], y[NI];
+            for (int i = 0; i < NI; ++i)
+              r[i] = bl[NI * i] - acc[i];
+            if constexpr (MODE == MODE_RESIDUAL)
+            {
+              int64_t g0, g1, g2;
+              origin(cur, p, g0, g1, g2);
+              T *rp = a.r + (g1 + 1) * m + (g0 + 1 + i0);
 #pragma unroll
-      for (int t = 0; t < NI; ++t)
-        v[t] = Z[NI * t];
-      mat_vec(P.S, v, y);
-      T *xp = a.x + (g1 + 1) * m + (g0 + 1 + i0);
+              for (int i = 0; i < NI; ++i)
+                rp[i * m] = r[i];
+            }
+          }
+          if constexpr (MODE != MODE_RESIDUAL)
+          {
+            T y[NI];
+            eo_st<K>(P.Se, P.So, r, y);
 #pragma unroll
-      for (int i = 0; i < NI; ++i)
-      {
-        if constexpr (MODE == MODE_BOUNDARY)
-          xp[i * m] = y[i];
-        else
-          xp[i * m] += y[i];
+            for (int c = 0; c < NI; ++c)
+              z[NI * c] = y[c];
+          }
+        }
       }
-    } while (0);
+      __syncthreads();
+      if (nxt < nbatch)
+      {
+        load_interior(cur ^ 1);
+        cp_async_commit();
+      }
+      if constexpr (MODE == MODE_RESIDUAL)
+        return;
+
+      // C: direction 0: S^T, scale, S
+      if (tid < PB * NI)
+      {
+        const int p = tid / NI;
+        const int i1 = tid - p * NI;
+        T *z = Z + p * ZW + NI * i1;
+        const T *inv = a.inv + NI * i1;
+        T v[NI], y[NI];
+#pragma unroll
+        for (int t = 0; t < NI; ++t)
+          v[t] = z[t];
+        eo_st<K>(P.Se, P.So, v, y);
+#pragma unroll
+        for (int t = 0; t < NI; ++t)
+          y[t] *= __ldg(inv + t);
+        eo_s<K>(P.Se, P.So, y, v);
+#pragma unroll
+        for (int t = 0; t < NI; ++t)
+          z[t] = v[t];
+      }
+      __syncthreads();
+
+      // D: direction 1: S, x^I update
+      if (tid < PB * NI)
+      {
+        const int p = tid / NI;
+        const int i0 = tid - p * NI;
+        const int gp = bt * PB + p;
+        if (gp < a.total)
+        {
+          int64_t g0, g1, g2;
+          origin(cur, p, g0, g1, g2);
+          const T *z = Z + p * ZW + i0;
+          T v[NI], y[NI];
+#pragma unroll
+          for (int t = 0; t < NI; ++t)
+            v[t] = z[NI * t];
+          eo_s<K>(P.Se, P.So, v, y);
+          T *xp = a.x + (g1 + 1) * m + (g0 + 1 + i0);
+#pragma unroll
+          for (int i = 0; i < NI; ++i)
+          {
+            if constexpr (MODE == MODE_BOUNDARY)
+              xp[i * m] = y[i];
+            else
+              xp[i * m] += y[i];
+          }
+        }
+      }
+    }
   }
+  cp_async_wait_all();
 }
 
 template <int D, int K, typename T, int MODE>
-void launch_vp_smooth(const PatchMats<T, K> &P, const ColorArgs<T> &a, cudaStream_t s)
+void launch_vp_smooth(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a, int sm_count, cudaStream_t s)
 {
-  constexpr int PB = sm_pb<D, K>(), NT = sm_nt<D, K>();
+  constexpr int PB = sm_pb<D, K, T>(), NT = sm_nt<D, K, T>();
   constexpr size_t smem = sm_smem_bytes<D, K, T>();
   static unsigned attr_mask = 0;
+  static int occupancy[32] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
   if (first_on_device(attr_mask))
   {
     check_cuda(cudaFuncSetAttribute(vp_smooth_kernel<D, K, T, MODE>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "cudaFuncSetAttribute(smoother)");
     check_cuda(cudaFuncSetAttribute(vp_smooth_kernel<D, K, T, MODE>,
                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100),
                "cudaFuncSetAttribute(smoother carveout)");
+    int occ = 0;
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vp_smooth_kernel<D, K, T, MODE>, NT, smem),
+               "occupancy(smoother)");
+    occupancy[dev & 31] = std::max(1, occ);
   }
-  const int grid = (a.total + PB - 1) / PB;
-  if (grid == 0)
+  const int nbatch = (a.total + PB - 1) / PB;
+  if (nbatch == 0)
     return;
+  const int grid = nbatch;  // one batch per CTA
+  (void)sm_count;
   vp_smooth_kernel<D, K, T, MODE><<<grid, NT, smem, s>>>(P, a);
   check_launch("vp_smooth_kernel");
 }
 
 template <int D, int K, typename T>
-void launch_vp_smooth_mode(const PatchMats<T, K> &P, const ColorArgs<T> &a, int mode,
+void launch_vp_smooth_mode(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a, int mode, int sm_count,
                            cudaStream_t s)
 {
   switch (mode)
   {
     case MODE_FUSED:
-      launch_vp_smooth<D, K, T, MODE_FUSED>(P, a, s);
+      launch_vp_smooth<D, K, T, MODE_FUSED>(P, a, sm_count, s);
       break;
     case MODE_BOUNDARY:
-      launch_vp_smooth<D, K, T, MODE_BOUNDARY>(P, a, s);
+      launch_vp_smooth<D, K, T, MODE_BOUNDARY>(P, a, sm_count, s);
       break;
     case MODE_RESIDUAL:
-      launch_vp_smooth<D, K, T, MODE_RESIDUAL>(P, a, s);
+      launch_vp_smooth<D, K, T, MODE_RESIDUAL>(P, a, sm_count, s);
       break;
     default:
-      launch_vp_smooth<D, K, T, MODE_SOLVE>(P, a, s);
+      launch_vp_smooth<D, K, T, MODE_SOLVE>(P, a, sm_count, s);
       break;
   }
 }
