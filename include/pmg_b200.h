@@ -157,6 +157,16 @@ int pmg_level_setup_data(pmg_level h, double *S, double *lambda, double *mass_if
                          double *stiff_if, double *prolongation, double *cell_mass,
                          double *cell_stiffness);
 
+/* Host-only, no device needed: the f64 setup of one level exactly as the
+ * library computes it (~ make_level_context, level_context.cpp:9-36, plus the
+ * derived band / even-odd data). Any pointer may be NULL. Sizes: S, ni*ni;
+ * lambda, ni; mass_if / stiff_if, ni*nc; prolongation, nc*(k+1); cell_*,
+ * (k+1)^2; band_*, k*(2k+1); eo_perm, ni (ni = 2k-1, nc = 2k+1). */
+int pmg_host_level_setup(int dim, int degree, int level, double *S, double *lambda,
+                         double *mass_if, double *stiff_if, double *prolongation,
+                         double *cell_mass, double *cell_stiffness, double *band_mass,
+                         double *band_stiff, int *eo_perm);
+
 /* Number of kernel launches issued by this library since load (counter). */
 int64_t pmg_launch_count(void);
 

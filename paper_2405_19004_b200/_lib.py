@@ -53,6 +53,7 @@ SIGNATURES = [
     ("pmg_l2_error_sin_host", _i, [_i, _i, _i, _pd, _pd]),
     ("pmg_gmres", _i, [_vp, _vp, _vp, _vp, _d, _i, _i, _pi, _pd, _i, _vp]),
     ("pmg_level_setup_data", _i, [_vp, _pd, _pd, _pd, _pd, _pd, _pd, _pd]),
+    ("pmg_host_level_setup", _i, [_i, _i, _i] + [_pd] * 9 + [_pi]),
     ("pmg_launch_count", _i64, []),
 ]
 

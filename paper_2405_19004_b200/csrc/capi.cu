@@ -647,6 +647,30 @@ int pmg_level_setup_data(pmg_level h, double *S, double *lambda, double *mass_if
   });
 }
 
+int pmg_host_level_setup(int dim, int degree, int level, double *S, double *lambda,
+                         double *mass_if, double *stiff_if, double *prolongation, double *cell_mass,
+                         double *cell_stiffness, double *band_mass, double *band_stiff, int *eo_perm)
+{
+  return guard([&] {
+    const LevelSetup s = make_level_setup(dim, degree, level);
+    auto cp = [](double *dst, const std::vector<double> &v) {
+      if (dst)
+        std::memcpy(dst, v.data(), v.size() * sizeof(double));
+    };
+    cp(S, s.S.a);
+    cp(lambda, s.lambda);
+    cp(mass_if, s.mass_if.a);
+    cp(stiff_if, s.stiff_if.a);
+    cp(prolongation, s.prolongation.a);
+    cp(cell_mass, s.cell_mass.a);
+    cp(cell_stiffness, s.cell_stiff.a);
+    cp(band_mass, s.band_mass);
+    cp(band_stiff, s.band_stiff);
+    if (eo_perm)
+      std::memcpy(eo_perm, s.eo_perm.data(), s.eo_perm.size() * sizeof(int));
+  });
+}
+
 int pmg_smooth(pmg_level h, int variant, void *x, const void *b, void *stream)
 {
   return guard([&] {
