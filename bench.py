@@ -15,9 +15,9 @@ since the C2 vectors (2 x 16 MiB) fit in the 126 MB L2; barrier +
 synchronize around the timed region, max over ranks. Clocks and throttle
 reasons are sampled with NVML during the timed region.
 
-Multi-GPU (torchrun, one process per GPU): the slab domain decomposition
-(paper_2405_19004_b200.dd) runs when the level is divisible across ranks;
-every rank owns an equal slab (weak scaling when --weak, strong otherwise).
+Multi-GPU (torchrun, one process per GPU, NCCL): weak scaling on a box of N
+stacked unit cubes along z (one cube's worth of DoFs per GPU), slab domain
+decomposition with per-colour halo planes (paper_2405_19004_b200/dd.py).
 """
 
 from __future__ import annotations
@@ -216,14 +216,25 @@ def main():
     import torch
 
     import paper_2405_19004_b200 as pmg
+    from paper_2405_19004_b200 import dd
 
     world, rank, local = dist_env()
+    # PMG_DD_SHARED_GPU=1: all ranks on cuda:0 over gloo with host-staged halo
+    # planes, to exercise the multi-rank path on a single-GPU box (test only)
+    shared = os.environ.get("PMG_DD_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dim != 3:
+            raise SystemExit("multi-GPU slab decomposition is 3D only")
 
     dt = np.float64 if args.dtype == "f64" else np.float32
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
@@ -231,21 +242,59 @@ def main():
     lib = pmg.load()
     ctx = pmg.make_multigrid_context(args.dim, args.degree, args.level, args.variant, dtype=dt, device=local)
     lev = ctx.levels[-1]
-    N = lev.level.total_dofs
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    x = torch.rand(N, dtype=tdt, device="cuda", generator=gen) * 2 - 1
-    b = torch.rand(N, dtype=tdt, device="cuda", generator=gen) * 2 - 1
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
+    if world == 1:
+        # the reference's unit cube on one GPU
+        N_total = lev.level.total_dofs
+        x = torch.rand(N_total, dtype=tdt, device="cuda", generator=gen) * 2 - 1
+        b = torch.rand(N_total, dtype=tdt, device="cuda", generator=gen) * 2 - 1
+
+        def step():
+            pmg.smooth(lev, x, b, args.variant)
+
+        colour_patch_counts = [colour_patches(args.dim, args.level, c) for c in range(1 << args.dim)]
+
+        def colour_launch(c):
+            pmg.smooth_color(lev, c, x, b, args.variant)
+    else:
+        # weak scaling: a stack of `world` unit cubes along z, one slab per
+        # rank, per-colour halo planes over NCCL overlapped with the interior
+        # patches (paper_2405_19004_b200/dd.py)
+        plan = dd.make_plan(world, rank, args.degree, args.level, stack=world)
+        N_total = plan.m * plan.m * plan.mz
+        x = torch.rand(plan.nplanes * plan.plane_size, dtype=tdt, device="cuda", generator=gen) * 2 - 1
+        b = torch.rand(plan.nplanes * plan.plane_size, dtype=tdt, device="cuda", generator=gen) * 2 - 1
+        comm = dd.StagedComm(x, plan.plane_size) if shared else dd.TorchDistComm(x, plan.plane_size)
+        smoother = dd.SlabSmoother(plan, dd.gpu_kernel(lev, plan, x, b, args.variant), comm)
+
+        def step():
+            smoother.smooth()
+
+        n = 1 << args.level
+        colour_patch_counts = []
+        for c in range(8):
+            zb = (c >> 2) & 1
+            nzv = sum(1 for v in range(plan.a, plan.b + 1) if v % 2 == zb)
+            cnt = nzv
+            for ax in range(2):
+                cnt *= n // 2 if (c >> ax) & 1 else n // 2 - 1
+            colour_patch_counts.append(cnt)
+
+        def colour_launch(c):
+            pmg.smooth_color_slab(lev, c, x, b, plan.lo, plan.nz, plan.a, plan.b, args.variant)
+
     def barrier():
+        torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
     # ---- warm-up --------------------------------------------------------------
     for _ in range(args.warmup):
-        pmg.smooth(lev, x, b, args.variant)
+        step()
     barrier()
 
     # ---- timed region: K steps, CUDA events per step, L2 flushed between ------
@@ -257,36 +306,39 @@ def main():
         for i in range(args.steps):
             flush.fill_(float(i))
             ev[i][0].record(stream)
-            pmg.smooth(lev, x, b, args.variant)
+            step()
             ev[i][1].record(stream)
         barrier()
     launches = lib.pmg_launch_count() - launches0
     t_step = sum(a.elapsed_time(c) for a, c in ev) / 1e3 / args.steps
     if dist is not None:
-        t = torch.tensor([t_step], dtype=torch.float64, device="cuda")
+        t = torch.tensor([t_step], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_step = float(t.item())
-    value = world * N / t_step
+    value = N_total / t_step
 
     # ---- per-launch roofline of the dominant kernel (the per-colour smoother) --
     F = flops_per_patch(args.dim, args.degree)
     colour_ms, colour_flops = 0.0, 0.0
     reps = max(3, min(20, args.steps))
     for c in range(1 << args.dim):
-        npatch = colour_patches(args.dim, args.level, c)
-        if npatch == 0:
+        if colour_patch_counts[c] == 0:
             continue
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         flush.fill_(0.5)
         e0.record(stream)
         for _ in range(reps):
-            pmg.smooth_color(lev, c, x, b, args.variant)
+            colour_launch(c)
         e1.record(stream)
         torch.cuda.synchronize()
         colour_ms += e0.elapsed_time(e1) / reps
-        colour_flops += F * npatch
+        colour_flops += F * colour_patch_counts[c]
     launch_s = colour_ms / 1e3
-    alg_bytes = algorithmic_bytes_per_step(args.dim, args.degree, args.level, word)
+    if world == 1:
+        alg_bytes = algorithmic_bytes_per_step(args.dim, args.degree, args.level, word)
+    else:  # this rank's slab: x read per colour + b^I read / x^I written per patch
+        alg_bytes = word * ((1 << args.dim) * plan.nplanes * plan.plane_size
+                            + 2 * sum(colour_patch_counts) * (2 * args.degree - 1) ** 3)
     peaks = json.load(open(MEASURED_PEAKS)) if os.path.exists(MEASURED_PEAKS) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
@@ -314,55 +366,84 @@ def main():
         "peak_source": f"{sm_count} SMs x {64 if args.dtype == 'f64' else 128} FMA/clk x 2 x {max_mhz} MHz",
     }
 
-    # ---- V-cycle throughput (secondary metric) ---------------------------------
-    li = args.level - 1
-    pmg.v_cycle(ctx, li, x, b, use_graph=True)
-    torch.cuda.synchronize()
-    vreps = max(3, min(10, args.steps))
-    vt = 0.0
-    for _ in range(vreps):
-        flush.fill_(1.0)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+    # ---- V-cycle throughput (secondary metric, single GPU) ---------------------
+    vcycle = None
+    if world == 1:
+        li = args.level - 1
         pmg.v_cycle(ctx, li, x, b, use_graph=True)
-        e1.record(stream)
         torch.cuda.synchronize()
-        vt += e0.elapsed_time(e1) / 1e3
-    vt /= vreps
+        vreps = max(3, min(10, args.steps))
+        vt = 0.0
+        for _ in range(vreps):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pmg.v_cycle(ctx, li, x, b, use_graph=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            vt += e0.elapsed_time(e1) / 1e3
+        vt /= vreps
+        vcycle = {"value": N_total / vt, "unit": "DoF/s", "ms": vt * 1e3, "cuda_graph": True}
 
-    # ---- e2e through the C-ABI with host buffers (pinned) ----------------------
-    xh = torch.empty(N, dtype=tdt, pin_memory=True).numpy()
-    bh = torch.empty(N, dtype=tdt, pin_memory=True).numpy()
-    xh[:] = x.cpu().numpy()
-    bh[:] = b.cpu().numpy()
-    for _ in range(2):
-        pmg.smooth(lev, xh, bh, args.variant)
+    # ---- e2e through the public API with host buffers (pinned) -----------------
     e2e_steps = max(3, min(args.steps, 20))
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        pmg.smooth(lev, xh, bh, args.variant)  # pmg_smooth_host: H2D x,b -> kernels -> D2H x
-    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    if world == 1:
+        xh = torch.empty(N_total, dtype=tdt, pin_memory=True).numpy()
+        bh = torch.empty(N_total, dtype=tdt, pin_memory=True).numpy()
+        xh[:] = x.cpu().numpy()
+        bh[:] = b.cpu().numpy()
+        for _ in range(2):
+            pmg.smooth(lev, xh, bh, args.variant)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            pmg.smooth(lev, xh, bh, args.variant)  # pmg_smooth_host: H2D x,b -> kernels -> D2H x
+        t_e2e = (time.perf_counter() - t0) / e2e_steps
+        h2d, d2h = 2 * N_total * word, N_total * word
+    else:
+        xh = torch.empty(x.numel(), dtype=tdt, pin_memory=True)
+        bh = torch.empty(b.numel(), dtype=tdt, pin_memory=True)
+        xh.copy_(x)
+        bh.copy_(b)
+        own = dd.owned_part(plan, x)
+        oh = torch.empty(own.numel(), dtype=tdt, pin_memory=True)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            x.copy_(xh, non_blocking=True)
+            b.copy_(bh, non_blocking=True)
+            step()
+            oh.copy_(dd.owned_part(plan, x), non_blocking=True)
+            torch.cuda.synchronize()
+        t_e2e = (time.perf_counter() - t0) / e2e_steps
+        h2d, d2h = (xh.numel() + bh.numel()) * word, oh.numel() * word
     if dist is not None:
-        t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        t = torch.tensor([t_e2e], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_e2e = float(t.item())
 
+    cfg = config_dict(args)
+    if world > 1:
+        cfg["workload"] = (f"3D Q{args.degree} box of {world} stacked unit cubes (2^{args.level} cells/dir each), "
+                           f"one {args.variant} smoother step, z-slab per GPU")
+        cfg["dofs"] = N_total
+        cfg["parallelism"] = f"slab decomposition x{world} (NCCL halo planes per colour)"
     out = {
         "metric": metric_name(args), "value": value, "unit": "DoF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
-        "data": "synthetic (x, b ~ U(-1,1))", "config": config_dict(args),
+        "data": "synthetic (x, b ~ U(-1,1))", "config": cfg,
         "roofline": roofline, "roofline_fp": roofline_fp,
-        "e2e": {"value": world * N / t_e2e, "unit": "DoF/s", "h2d_bytes_per_step": 2 * N * word,
-                "d2h_bytes_per_step": N * word, "api": "pmg_smooth_host (C-ABI, pinned host buffers)"},
+        "e2e": {"value": N_total / t_e2e, "unit": "DoF/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "api": "pmg_smooth_host (C-ABI, pinned host buffers)" if world == 1 else
+                       "slab H2D, SlabSmoother.smooth, owned-plane D2H (pinned)"},
         "clocks": sampler.summary(), "gpu_launches": int(launches),
-        "vcycle": {"value": world * N / vt, "unit": "DoF/s", "ms": vt * 1e3, "cuda_graph": True},
     }
-    if dist is not None:
-        out["parallelism"] = f"replicas x{world}"
+    if vcycle is not None:
+        out["vcycle"] = vcycle
 
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         v, done, threads, tcpu = cpu_reference_run(args, 10 ** 6, 1, args.cpu_budget)
         out["cpu_baseline"] = {"value": v, "unit": "DoF/s", "cores": threads, "kind": "reference",
                                "sample": f"{done} full smoothing steps of the same workload in {tcpu:.1f} s "

@@ -84,6 +84,16 @@ int pmg_smooth_host(pmg_level h, int variant, void *x, const void *b);
 int pmg_smooth_color(pmg_level h, int variant, int color, void *x, const void *b,
                      void *stream);
 
+/* One colour restricted to a slab of a (possibly stacked) 3D box, for the
+ * multi-GPU domain decomposition (paper_2405_19004_b200/dd.py): the box has
+ * the level's n cells along x, y and nz_cells along z; only patches whose
+ * vertex z-coordinate lies in [vz_lo, vz_hi] are smoothed; x_local / b_local
+ * hold the global dof planes z >= z_offset (m*m values per plane). fused or
+ * boundary variant. */
+int pmg_smooth_color_slab(pmg_level h, int variant, int color, void *x_local,
+                          const void *b_local, int64_t z_offset, int64_t nz_cells, int vz_lo,
+                          int vz_hi, void *stream);
+
 /* ~ apply_laplacian<T>(level, cell_mass, cell_stiffness, x, y, mode, threads)
  *   operator.hpp:47-50 — y = A_l x. */
 int pmg_apply_laplacian(pmg_level h, const void *x, void *y, void *stream);

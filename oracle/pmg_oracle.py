@@ -484,6 +484,39 @@ def smooth(ctx: LevelContext, x: np.ndarray, b: np.ndarray, variant: str = "fuse
     return xp[(slice(1, m + 1),) * d].reshape(-1).copy()
 
 
+def smooth_colour_slab(ctx: LevelContext, x_loc: np.ndarray, b_loc: np.ndarray, color: int, zoff: int,
+                       nz_cells: int, vz_lo: int, vz_hi: int) -> None:
+    """One colour of the fused smoother (smoother.cpp:109-126) restricted to the
+    patches with vertex z in [vz_lo, vz_hi] of a 3D box with the level's n
+    cells along x, y and nz_cells along z (a stacked box when nz_cells != n);
+    x_loc / b_loc hold the global dof planes z >= zoff. In place on x_loc.
+    Checker for the slab decomposition (paper_2405_19004_b200/dd.py)."""
+    lev = ctx.level
+    assert lev.dim == 3
+    k, n, m = lev.degree, lev.cells_per_dim, lev.dofs_per_dim
+    nloc = x_loc.size // (m * m)
+    if any(len(_colour_vertices(n, (color >> a) & 1)) == 0 for a in range(2)):
+        return
+    vz = np.array([v for v in range(vz_lo, vz_hi + 1) if v % 2 == ((color >> 2) & 1)], dtype=int)
+    if vz.size == 0:
+        return
+    xp = np.zeros((nloc + 2, m + 2, m + 2), dtype=x_loc.dtype)
+    bp = np.zeros_like(xp)
+    xp[1:-1, 1:-1, 1:-1] = x_loc.reshape(nloc, m, m)
+    bp[1:-1, 1:-1, 1:-1] = b_loc.reshape(nloc, m, m)
+    cl = _colour_index_arrays(lev, color, 0, 2 * k)[:2]
+    it = _colour_index_arrays(lev, color, 1, 2 * k - 1)[:2]
+    # z lattice index p = k (v - 1) + t, local padded plane p - zoff
+    cl.append(k * (vz[:, None] - 1) + np.arange(0, 2 * k + 1)[None, :] - zoff)
+    it.append(k * (vz[:, None] - 1) + np.arange(1, 2 * k)[None, :] - zoff)
+    assert cl[2].min() >= 0 and cl[2].max() <= nloc + 1
+    u = _gather(xp, cl, 3)
+    bi = _gather(bp, it, 3)
+    v = apply_patch_inverse(ctx.fastdiag, bi - apply_patch_operator(ctx.patch, 3, u))
+    # write back ONLY the patch interiors (other planes may be in flight)
+    _scatter(x_loc.reshape(nloc, m, m), [i - 1 for i in it], 3, v, "add")
+
+
 # ---------------------------------------------------------------------------
 # operator (operator.cpp:122-185, 283-411)
 # ---------------------------------------------------------------------------

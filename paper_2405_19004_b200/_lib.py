@@ -30,6 +30,7 @@ SIGNATURES = [
     ("pmg_smooth", _i, [_vp, _i, _vp, _vp, _vp]),
     ("pmg_smooth_host", _i, [_vp, _i, _vp, _vp]),
     ("pmg_smooth_color", _i, [_vp, _i, _i, _vp, _vp, _vp]),
+    ("pmg_smooth_color_slab", _i, [_vp, _i, _i, _vp, _vp, _i64, _i64, _i, _i, _vp]),
     ("pmg_apply_laplacian", _i, [_vp, _vp, _vp, _vp]),
     ("pmg_apply_laplacian_host", _i, [_vp, _vp, _vp]),
     ("pmg_compute_residual", _i, [_vp, _vp, _vp, _vp, _vp]),

@@ -228,6 +228,30 @@ ColorArgs<T> color_args(const pmg_level_s *l, int color, T *x, const T *b)
     }
     a.total *= a.np[q];
   }
+  a.mz = a.m;
+  a.zoff = 0;
+  return a;
+}
+
+// Colour `color` restricted to the slab of vertex planes vz in [vz_lo, vz_hi]
+// (last direction) of a box with nz_cells cells along z (a stacked box when
+// nz_cells != n); x / b hold the global dof planes starting at zoff.
+template <typename T>
+ColorArgs<T> color_args_slab(const pmg_level_s *l, int color, T *x, const T *b, int64_t zoff,
+                             int64_t nz_cells, int vz_lo, int vz_hi)
+{
+  if (l->S.dim != 3)
+    throw InvalidArg("slab decomposition is implemented for dim 3");
+  if (nz_cells < 2 || vz_lo < 1 || vz_hi > nz_cells - 1 || zoff < 0)
+    throw InvalidArg("slab: invalid vertex range / box");
+  ColorArgs<T> a = color_args<T>(l, color, x, b);
+  const int bit = (color >> 2) & 1;
+  int first = vz_lo + (((vz_lo & 1) != bit) ? 1 : 0);
+  a.np[2] = first > vz_hi ? 0 : (vz_hi - first) / 2 + 1;
+  a.vb[2] = first;
+  a.total = a.np[0] * a.np[1] * a.np[2];
+  a.mz = nz_cells * l->S.k - 1;
+  a.zoff = zoff;
   return a;
 }
 
@@ -280,6 +304,22 @@ void smooth_color_impl(pmg_level_s *l, int variant, int color, T *x, const T *b,
     default:
       throw InvalidArg("smooth: unknown variant " + std::to_string(variant));
   }
+}
+
+template <typename T>
+void smooth_color_slab_impl(pmg_level_s *l, int variant, int color, T *x, const T *b, int64_t zoff,
+                            int64_t nz_cells, int vz_lo, int vz_hi, cudaStream_t s)
+{
+  ColorArgs<T> a = color_args_slab<T>(l, color, x, b, zoff, nz_cells, vz_lo, vz_hi);
+  if (a.total == 0)
+    return;
+  const auto &kt = ktab<T>(l);
+  if (variant == PMG_FUSED)
+    kt.smooth(l->patch_mats.data(), a, MODE_FUSED, l->sm_count, s);
+  else if (variant == PMG_BOUNDARY)
+    kt.smooth(l->patch_mats.data(), a, MODE_BOUNDARY, l->sm_count, s);
+  else
+    throw InvalidArg("slab smoother: fused or boundary variant only");
 }
 
 template <typename T>
@@ -690,6 +730,20 @@ int pmg_smooth_color(pmg_level h, int variant, int color, void *x, const void *b
     DeviceGuard dg(h->device);
     PMG_DISPATCH_T(h, smooth_color_impl<T>(h, variant, color, static_cast<T *>(x),
                                            static_cast<const T *>(b), as_stream(stream)));
+  });
+}
+
+int pmg_smooth_color_slab(pmg_level h, int variant, int color, void *x_local, const void *b_local,
+                          int64_t z_offset, int64_t nz_cells, int vz_lo, int vz_hi, void *stream)
+{
+  return guard([&] {
+    require_level(h);
+    if (color < 0 || color >= (1 << h->S.dim))
+      throw InvalidArg("colour out of range");
+    DeviceGuard dg(h->device);
+    PMG_DISPATCH_T(h, smooth_color_slab_impl<T>(h, variant, color, static_cast<T *>(x_local),
+                                                static_cast<const T *>(b_local), z_offset, nz_cells,
+                                                vz_lo, vz_hi, as_stream(stream)));
   });
 }
 

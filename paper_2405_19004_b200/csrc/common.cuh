@@ -113,7 +113,9 @@ struct ColorArgs
   const T *b;     // right-hand side
   T *r;           // global residual buffer (MODE_RESIDUAL output / MODE_SOLVE input)
   const T *inv;   // inverse eigenvalue sums, (2K-1)^D, direction 0 fastest
-  int64_t m;      // dofs per direction
+  int64_t m;      // dofs per direction (directions 0 .. d-2)
+  int64_t mz;     // dofs along the last direction of the (possibly stacked) global box
+  int64_t zoff;   // global last-direction dof index of plane 0 of x / b / r (slab offset)
   int np[3];      // patches of this colour per direction
   int vb[3];      // vertex coordinate v_a = 2 j_a + vb[a]
   int total;      // patches in this colour

@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
       const int y0 = org[slot][p][0] + t0, y1 = org[slot][p][1] + t1, y2 = org[slot][p][2] + t2;
       bool ok = static_cast<uint32_t>(y0) < static_cast<uint32_t>(m) &&
                 static_cast<uint32_t>(y1) < static_cast<uint32_t>(m) &&
-                (D == 2 || static_cast<uint32_t>(y2) < static_cast<uint32_t>(m));
+                (D == 2 || static_cast<uint64_t>(y2) < static_cast<uint64_t>(a.mz));
       if constexpr (MODE == MODE_BOUNDARY)
       {
         // boundary variant never reads x^I (smoother.cpp:128-148)
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
                            (D == 2 || (t2 >= 1 && t2 <= NC - 2));
         ok = ok && !inner;
       }
-      const int64_t gi = (D == 3) ? (static_cast<int64_t>(y2) * m + y1) * m + y0 : static_cast<int64_t>(y1) * m + y0;
+      const int64_t gi = (D == 3) ? (static_cast<int64_t>(y2 - a.zoff) * m + y1) * m + y0 : static_cast<int64_t>(y1) * m + y0;
       cp_async_elem(U + p * UW + r, ok ? a.x + gi : a.x, ok);
     }
   };
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
       const int g0 = org[slot][p][0];
       const bool ok = g0 > -(1 << 29);
       const int64_t y0 = g0 + 1 + i0, y1 = org[slot][p][1] + 1 + i1, y2 = org[slot][p][2] + 1 + i2;
-      const int64_t gi = (D == 3) ? (y2 * m + y1) * m + y0 : y1 * m + y0;
+      const int64_t gi = (D == 3) ? ((y2 - a.zoff) * m + y1) * m + y0 : y1 * m + y0;
       cp_async_elem(Bs + p * BW + r, ok ? vec + gi : a.x, ok);
     }
   };
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
             {
               int64_t g0, g1, g2;
               origin(cur, p, g0, g1, g2);
-              T *rp = a.r + ((g2 + 1) * m + (g1 + 1 + i1)) * m + (g0 + 1 + i0);
+              T *rp = a.r + ((g2 + 1 - a.zoff) * m + (g1 + 1 + i1)) * m + (g0 + 1 + i0);
 #pragma unroll
               for (int i = 0; i < NI; ++i)
                 rp[i * m2] = r[i];
@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
           for (int t = 0; t < NI; ++t)
             v[t] = z[NI * NC * t];
           eo_s<K>(P.Se, P.So, v, y);
-          T *xp = a.x + ((g2 + 1) * m + (g1 + 1 + i1)) * m + (g0 + 1 + i0);
+          T *xp = a.x + ((g2 + 1 - a.zoff) * m + (g1 + 1 + i1)) * m + (g0 + 1 + i0);
 #pragma unroll
           for (int i = 0; i < NI; ++i)
           {

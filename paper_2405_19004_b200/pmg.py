@@ -33,7 +33,7 @@ from ._lib import PMG_F32, PMG_F64, VARIANTS, DivergenceError, check
 
 __all__ = [
     "CartesianLevel", "build_hierarchy", "dof_index", "LevelContext", "make_level_context",
-    "MultigridContext", "make_multigrid_context", "SmootherVariant", "smooth", "smooth_color",
+    "MultigridContext", "make_multigrid_context", "SmootherVariant", "smooth", "smooth_color", "smooth_color_slab",
     "apply_laplacian", "compute_residual", "prolongate", "restrict_vector", "v_cycle",
     "full_multigrid", "FmgStats", "vector_norm", "compute_rhs", "l2_error", "gmres", "SolveStats",
     "DivergenceError",
@@ -256,6 +256,22 @@ def smooth_color(ctx: LevelContext, color: int, x, b, variant="fused") -> None:
         raise ValueError("smooth_color: device (torch CUDA) vectors only")
     check(_lib.load().pmg_smooth_color(ctx.handle, _variant_code(variant), color, xa.ptr, ba.ptr,
                                        _stream((xa, ba))), "smooth_color")
+
+
+def smooth_color_slab(ctx: LevelContext, color: int, x_local, b_local, z_offset: int, nz_cells: int,
+                      vz_lo: int, vz_hi: int, variant="fused") -> None:
+    """One colour on a z-slab of a (possibly stacked) 3D box (device vectors
+    holding the global dof planes z >= z_offset); see dd.py."""
+    lev = ctx.level
+    plane = lev.dofs_per_dim ** 2
+    for name, v in (("x_local", x_local), ("b_local", b_local)):
+        if not _is_torch(v) or not v.is_cuda or v.numel() % plane:
+            raise ValueError(f"{name}: device vector of whole dof planes required")
+    xa = _Arr(x_local, x_local.numel(), ctx._code, "x_local", True)
+    ba = _Arr(b_local, b_local.numel(), ctx._code, "b_local", False)
+    check(_lib.load().pmg_smooth_color_slab(ctx.handle, _variant_code(variant), color, xa.ptr, ba.ptr,
+                                            int(z_offset), int(nz_cells), int(vz_lo), int(vz_hi),
+                                            _stream((xa,))), "smooth_color_slab")
 
 
 def apply_laplacian(ctx: LevelContext, x, y, mode: str = "colored", threads: int = 1) -> None:

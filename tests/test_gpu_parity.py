@@ -208,3 +208,32 @@ def test_determinism(pmg, cuda):
         pmg.v_cycle(ctx, 2, xd, dev(cuda, b))
         outs.append(xd.cpu().numpy())
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("world,k,level,stack", [(2, 2, 4, 1), (4, 3, 3, 1), (3, 1, 5, 1), (8, 2, 4, 1),
+                                                 (2, 4, 3, 2), (4, 2, 3, 4)])
+def test_slab_decomposition_virtual_ranks(pmg, cuda, world, k, level, stack):
+    """P slabs (virtual ranks on one GPU, plane copies in place
+    of NCCL) give BITWISE the single-domain GPU result; for the unit cube that
+    is also the reference's smooth."""
+    from paper_2405_19004_b200 import dd
+
+    ctx = pmg.make_multigrid_context(3, k, level)
+    lev = ctx.levels[-1]
+    full = dd.make_plan(1, 0, k, level, stack)
+    n = full.nplanes * full.plane_size
+    x0, b = refbind.fill_uniform(42, n, n)
+    xg, bg = dev(cuda, x0.copy()), dev(cuda, b)
+    dd.virtual_smooth([full], [dd.gpu_kernel(lev, full, xg, bg)], [xg])
+    ps = [dd.make_plan(world, r, k, level, stack) for r in range(world)]
+    xs = [dd.scatter_global(p, dev(cuda, x0)).clone() for p in ps]
+    bs = [dd.scatter_global(p, bg).clone() for p in ps]
+    dd.virtual_smooth(ps, [dd.gpu_kernel(lev, p, x, bb) for p, x, bb in zip(ps, xs, bs)], xs)
+    got = cuda.cat([dd.owned_part(p, x) for p, x in zip(ps, xs)])
+    assert cuda.equal(got, xg)
+    if stack == 1:
+        xs1 = dev(cuda, x0.copy())
+        pmg.smooth(lev, xs1, bg)
+        assert cuda.equal(xs1, xg)
+        ref = refbind.RefMg(3, k, level)
+        assert rel(xg.cpu().numpy(), ref.smooth(level - 1, x0, b)) < 1e-12
