@@ -328,43 +328,61 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
     }
   };
 
-  // prefetch the closure of the batch whose origins are in `slot` into U
-  // (coalesced, zero-filled outside the domain)
+  // Cooperative cp.async loads, one z-line (3D; y-line in 2D) per thread:
+  // thread -> (patch, t0, t1) once, then a fixed-stride walk along the last
+  // direction, so the per-element cost is an address increment plus one
+  // bounds test. Lanes run along x: row segments are contiguous in HBM.
   auto load_closure = [&](int slot) {
-#pragma unroll 1
-    for (int e = tid; e < PB * NCD; e += NT)
+    constexpr int LINES = PB * (D == 3 ? NC * NC : NC);
+    if (tid >= LINES)
+      return;
+    const int p = tid / (D == 3 ? NC * NC : NC);
+    const int rr = tid - p * (D == 3 ? NC * NC : NC);
+    const int t0 = rr % NC, t1 = (D == 3) ? rr / NC : 0;
+    const int y0 = org[slot][p][0] + t0;
+    const int y1 = org[slot][p][1] + ((D == 3) ? t1 : 0);
+    const int ylast0 = org[slot][p][D == 3 ? 2 : 1];
+    const bool inplane = static_cast<uint32_t>(y0) < static_cast<uint32_t>(m) &&
+                         (D == 2 || static_cast<uint32_t>(y1) < static_cast<uint32_t>(m));
+    const int64_t step = (D == 3) ? m * m : m;
+    const int64_t base = (D == 3) ? static_cast<int64_t>(y1) * m + y0 : static_cast<int64_t>(y0);
+    const int64_t zl = (D == 3) ? a.zoff : 0;
+    const int64_t mlast = (D == 3) ? a.mz : m;
+    T *dst = U + p * UW + rr;
+#pragma unroll
+    for (int t = 0; t < NC; ++t)
     {
-      const int p = e / NCD, r = e - (e / NCD) * NCD;
-      const int t0 = r % NC, t1 = (r / NC) % NC, t2 = (D == 3) ? r / (NC * NC) : 0;
-      const int y0 = org[slot][p][0] + t0, y1 = org[slot][p][1] + t1, y2 = org[slot][p][2] + t2;
-      bool ok = static_cast<uint32_t>(y0) < static_cast<uint32_t>(m) &&
-                static_cast<uint32_t>(y1) < static_cast<uint32_t>(m) &&
-                (D == 2 || static_cast<uint64_t>(y2) < static_cast<uint64_t>(a.mz));
+      const int yl = ylast0 + t;
+      bool ok = inplane && static_cast<uint64_t>(static_cast<int64_t>(yl)) < static_cast<uint64_t>(mlast);
       if constexpr (MODE == MODE_BOUNDARY)
       {
         // boundary variant never reads x^I (smoother.cpp:128-148)
-        const bool inner = t0 >= 1 && t0 <= NC - 2 && t1 >= 1 && t1 <= NC - 2 &&
-                           (D == 2 || (t2 >= 1 && t2 <= NC - 2));
+        const bool inner = t0 >= 1 && t0 <= NC - 2 && t >= 1 && t <= NC - 2 &&
+                           (D == 2 || (t1 >= 1 && t1 <= NC - 2));
         ok = ok && !inner;
       }
-      const int64_t gi = (D == 3) ? (static_cast<int64_t>(y2 - a.zoff) * m + y1) * m + y0 : static_cast<int64_t>(y1) * m + y0;
-      cp_async_elem(U + p * UW + r, ok ? a.x + gi : a.x, ok);
+      cp_async_elem(dst + (D == 3 ? NC * NC : NC) * t, ok ? a.x + base + (yl - zl) * step : a.x, ok);
     }
   };
   // prefetch the interior of b (or of the residual for MODE_SOLVE)
   auto load_interior = [&](int slot) {
+    constexpr int LINES = PB * (D == 3 ? NI * NI : NI);
+    if (tid >= LINES)
+      return;
     const T *vec = (MODE == MODE_SOLVE) ? a.r : a.b;
-#pragma unroll 1
-    for (int e = tid; e < PB * NID; e += NT)
-    {
-      const int p = e / NID, r = e - (e / NID) * NID;
-      const int i0 = r % NI, i1 = (r / NI) % NI, i2 = (D == 3) ? r / (NI * NI) : 0;
-      const int g0 = org[slot][p][0];
-      const bool ok = g0 > -(1 << 29);
-      const int64_t y0 = g0 + 1 + i0, y1 = org[slot][p][1] + 1 + i1, y2 = org[slot][p][2] + 1 + i2;
-      const int64_t gi = (D == 3) ? ((y2 - a.zoff) * m + y1) * m + y0 : y1 * m + y0;
-      cp_async_elem(Bs + p * BW + r, ok ? vec + gi : a.x, ok);
-    }
+    const int p = tid / (D == 3 ? NI * NI : NI);
+    const int rr = tid - p * (D == 3 ? NI * NI : NI);
+    const int i0 = rr % NI, i1 = (D == 3) ? rr / NI : 0;
+    const int g0 = org[slot][p][0];
+    const bool ok = g0 > -(1 << 29);
+    const int64_t step = (D == 3) ? m * m : m;
+    const int64_t base = (D == 3) ? static_cast<int64_t>(org[slot][p][1] + 1 + i1) * m + (g0 + 1 + i0)
+                                  : static_cast<int64_t>(g0 + 1 + i0);
+    const int64_t z0 = static_cast<int64_t>(org[slot][p][D == 3 ? 2 : 1]) + 1 - ((D == 3) ? a.zoff : 0);
+    T *dst = Bs + p * BW + rr;
+#pragma unroll
+    for (int t = 0; t < NI; ++t)
+      cp_async_elem(dst + (D == 3 ? NI * NI : NI) * t, ok ? vec + base + (z0 + t) * step : a.x, ok);
   };
   auto origin = [&](int slot, int p, int64_t &g0, int64_t &g1, int64_t &g2) {
     g0 = org[slot][p][0];
@@ -605,11 +623,16 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
             v[t] = z[NI * NC * t];
           eo_s<K>(P.Se, P.So, v, y);
           T *xp = a.x + ((g2 + 1 - a.zoff) * m + (g1 + 1 + i1)) * m + (g0 + 1 + i0);
+          // x^I old values are still in the staged closure (no other patch of
+          // this colour writes them), so the update is a pure store
+          const T *xo = U + p * UW + (1 + i0) + NC * (1 + i1) + NC * NC;
 #pragma unroll
           for (int i = 0; i < NI; ++i)
           {
             if constexpr (MODE == MODE_BOUNDARY)
               xp[i * m2] = y[i];
+            else if constexpr (MODE == MODE_FUSED)
+              xp[i * m2] = xo[NC * NC * i] + y[i];
             else
               xp[i * m2] += y[i];
           }
@@ -754,11 +777,14 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
             v[t] = z[NI * t];
           eo_s<K>(P.Se, P.So, v, y);
           T *xp = a.x + (g1 + 1) * m + (g0 + 1 + i0);
+          const T *xo = U + p * UW + (1 + i0) + NC;
 #pragma unroll
           for (int i = 0; i < NI; ++i)
           {
             if constexpr (MODE == MODE_BOUNDARY)
               xp[i * m] = y[i];
+            else if constexpr (MODE == MODE_FUSED)
+              xp[i * m] = xo[NC * i] + y[i];
             else
               xp[i * m] += y[i];
           }
