@@ -237,3 +237,16 @@ def test_slab_decomposition_virtual_ranks(pmg, cuda, world, k, level, stack):
         assert cuda.equal(xs1, xg)
         ref = refbind.RefMg(3, k, level)
         assert rel(xg.cpu().numpy(), ref.smooth(level - 1, x0, b)) < 1e-12
+
+
+def test_cpp_shim(pmg, cuda):
+    """C++ host code (include/pmg_b200.hpp over the C-ABI) vs the reference."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "_bin", "shim_parity")
+    if not os.path.exists(exe):
+        pytest.fail("tests/cpp/_bin/shim_parity missing: run __graft_entry__.build()")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "OK" in out.stdout
