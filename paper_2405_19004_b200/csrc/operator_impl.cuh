@@ -4,13 +4,19 @@
 // and compute_residual<T> (multigrid.cpp:268-276). The reference loops over
 // cells in 2^d parity colours and scatter-adds cell contributions. On a
 // uniform Cartesian level the operator is exactly the Kronecker sum of the
-// global 1D banded mass/stiffness matrices (the identity the reference's own
+// global banded 1D mass/stiffness matrices (the identity the reference's own
 // CSR oracle relies on, operator.cpp:194-281), so the device kernel is a
-// node-centric, deterministic (no atomics) sum factorisation:
-//   3D: zM = M0 x, zA = A0 x (direction 0, smem tile with halo k)
-//       wMM = M1 zM, wS = A1 zM + M1 zA (direction 1, smem tile)
-//       y  = A2 wMM + M2 wS (direction 2, streamed through a per-thread ring
-//            of 2k+1 planes while the CTA marches along z)
+// node-centric, deterministic (no atomics) sum factorisation, streamed
+// through the last direction:
+//   3D, per z-plane q of the input:
+//     dir 0: zM = M0 x, zA = A0 x     (x tile with a k-halo, cp.async, smem)
+//     dir 1: wM = M1 zM, wS = A1 zM + M1 zA   (registers)
+//     dir 2: every output plane p in [q-k, q+k] accumulates
+//            A2[p][q] wM + M2[p][q] wS into a register ring of 2k+1 planes
+//            (the plane loop is unrolled by 2k+1 so ring slots are static);
+//            plane q-k is complete and is written (r = b - acc fused).
+//   One barrier per plane: the x tile and the dir-0 results are double
+//   buffered and the next plane's tile is fetched while this one computes.
 // Band coefficients depend only on the lattice residue p mod k.
 #pragma once
 
@@ -22,15 +28,27 @@ namespace pmgb
 template <int K, typename T>
 constexpr int op_t1()
 {
-  return (K * static_cast<int>(sizeof(T)) >= 40) ? 4 : 8;
+  return 8;
 }
 
 template <int K, typename T>
 constexpr size_t op3d_smem()
 {
-  constexpr int T0 = 32, T1 = op_t1<K, T>(), NT = T0 * T1, W = 2 * K + 1;
+  constexpr int T0 = 32, T1 = op_t1<K, T>(), W = 2 * K + 1;
   constexpr int XW = T0 + 2 * K, XH = T1 + 2 * K;
-  return sizeof(T) * (static_cast<size_t>(XH) * XW + 2 * XH * T0 + 2 * W * NT + 2 * K * W);
+  return sizeof(T) * (2 * static_cast<size_t>(XH) * XW + 4 * XH * T0 + 2 * K * W);
+}
+
+template <typename T>
+__device__ __forceinline__ void op_cp_async(T *smem, const T *gmem, bool valid)
+{
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 4 : 0)
+                 : "memory");
 }
 
 template <int K, typename T, bool RESID>
@@ -40,13 +58,12 @@ __global__ void __launch_bounds__(32 * op_t1<K, T>())
 {
   constexpr int T0 = 32, T1 = op_t1<K, T>(), NT = T0 * T1, W = 2 * K + 1, R = 2 * K + 1;
   constexpr int XW = T0 + 2 * K, XH = T1 + 2 * K;
+  constexpr int ROWS = (XH + T1 - 1) / T1;  // dir-0 rows per thread
   extern __shared__ __align__(16) unsigned char smraw[];
-  T *Xs = reinterpret_cast<T *>(smraw);
-  T *ZM = Xs + XH * XW;
-  T *ZA = ZM + XH * T0;
-  T *RM = ZA + XH * T0;
-  T *RS = RM + R * NT;
-  T *bm = RS + R * NT;
+  T *Xs = reinterpret_cast<T *>(smraw);  // [2][XH][XW]
+  T *ZM = Xs + 2 * XH * XW;              // [2][XH][T0]
+  T *ZA = ZM + 2 * XH * T0;              // [2][XH][T0]
+  T *bm = ZA + 2 * XH * T0;              // [K][W]
   T *ba = bm + K * W;
 
   const int tid = threadIdx.x;
@@ -60,88 +77,128 @@ __global__ void __launch_bounds__(32 * op_t1<K, T>())
   const int64_t zs = static_cast<int64_t>(blockIdx.z) * zchunk;
   const int64_t ze = min(zs + zchunk, m);
   const int i = tid % T0, jj = tid / T0;
-  const int res0 = static_cast<int>((g0 + i + 1) % K);
-  const int res1 = static_cast<int>((g1 + jj + 1) % K);
   __syncthreads();
   T c0m[W], c0a[W], c1m[W], c1a[W];
-#pragma unroll
-  for (int o = 0; o < W; ++o)
   {
-    c0m[o] = bm[res0 * W + o];
-    c0a[o] = ba[res0 * W + o];
-    c1m[o] = bm[res1 * W + o];
-    c1a[o] = ba[res1 * W + o];
+    const int res0 = static_cast<int>((g0 + i + 1) % K);
+    const int res1 = static_cast<int>((g1 + jj + 1) % K);
+#pragma unroll
+    for (int o = 0; o < W; ++o)
+    {
+      c0m[o] = bm[res0 * W + o];
+      c0a[o] = ba[res0 * W + o];
+      c1m[o] = bm[res1 * W + o];
+      c1a[o] = ba[res1 * W + o];
+    }
   }
   const bool out_ok = (g0 + i < m) && (g1 + jj < m);
 
-  int slot = 0;  // ring slot of plane q2
-  for (int64_t q2 = zs - K; q2 < ze + K; ++q2)
-  {
-    const bool zin = q2 >= 0 && q2 < m;
+  // x tile of input plane q (zero outside the domain) into buffer `buf`
+  auto load_plane = [&](int64_t q, int buf) {
+    const bool zin = q >= 0 && q < m;
+    T *dst = Xs + buf * XH * XW;
     for (int e = tid; e < XH * XW; e += NT)
     {
       const int jr = e / XW, ir = e - jr * XW;
       const int64_t gx = g0 - K + ir, gy = g1 - K + jr;
-      T v = T(0);
-      if (zin && gx >= 0 && gx < m && gy >= 0 && gy < m)
-        v = __ldg(x + (q2 * m + gy) * m + gx);
-      Xs[e] = v;
+      const bool ok = zin && gx >= 0 && gx < m && gy >= 0 && gy < m;
+      op_cp_async(dst + e, ok ? x + (q * m + gy) * m + gx : x, ok);
     }
-    __syncthreads();
-    for (int j = jj; j < XH; j += T1)
-    {
-      const T *xr = Xs + j * XW + i;
-      T zm = c0m[0] * xr[0], za = c0a[0] * xr[0];
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  const int NPL = static_cast<int>(ze - zs) + 2 * K;  // input planes zs-K .. ze+K-1
+  T acc[R];
 #pragma unroll
-      for (int o = 1; o < W; ++o)
-      {
-        zm = fma(c0m[o], xr[o], zm);
-        za = fma(c0a[o], xr[o], za);
-      }
-      ZM[j * T0 + i] = zm;
-      ZA[j * T0 + i] = za;
-    }
-    __syncthreads();
-    {
-      T wm = T(0), ws = T(0);
+  for (int o = 0; o < R; ++o)
+    acc[o] = T(0);
+
+  load_plane(zs - K, 0);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+
+  for (int base = 0; base < NPL; base += R)
+  {
 #pragma unroll
-      for (int o = 0; o < W; ++o)
-      {
-        const T zm = ZM[(jj + o) * T0 + i], za = ZA[(jj + o) * T0 + i];
-        wm = fma(c1m[o], zm, wm);
-        ws = fma(c1a[o], zm, ws);
-        ws = fma(c1m[o], za, ws);
-      }
-      RM[slot * NT + tid] = wm;
-      RS[slot * NT + tid] = ws;
-    }
-    const int64_t g2 = q2 - K;
-    if (g2 >= zs)
+    for (int u = 0; u < R; ++u)
     {
-      const int res2 = static_cast<int>((g2 + 1) % K);
-      T acc = T(0);
-      int s = slot + 1;
-      if (s == R)
-        s = 0;
-#pragma unroll
-      for (int o = 0; o < W; ++o)
+      const int it = base + u;  // uniform across the CTA
+      if (it < NPL)
       {
-        acc = fma(ba[res2 * W + o], RM[s * NT + tid], acc);
-        acc = fma(bm[res2 * W + o], RS[s * NT + tid], acc);
-        if (++s == R)
-          s = 0;
-      }
-      if (out_ok)
-      {
-        const int64_t idx = (g2 * m + g1 + jj) * m + g0 + i;
+        const int buf = it & 1;
+        const int64_t q = zs - K + it;
+        if (it + 1 < NPL)
+          load_plane(q + 1, buf ^ 1);
+        // output plane emitted this iteration (inputs up to q are in)
+        const int64_t p_out = q - K;
+        const bool emit = it >= 2 * K && p_out < ze;
+        T bval = T(0);
         if constexpr (RESID)
-          y[idx] = __ldg(b + idx) - acc;
-        else
-          y[idx] = acc;
+        {
+          if (emit && out_ok)
+            bval = __ldg(b + (p_out * m + g1 + jj) * m + g0 + i);
+        }
+        // dir 0: rows jj, jj+T1, ... of the tile
+        const T *xs = Xs + buf * XH * XW;
+        T *zm = ZM + buf * XH * T0;
+        T *za = ZA + buf * XH * T0;
+#pragma unroll
+        for (int rr = 0; rr < ROWS; ++rr)
+        {
+          const int j = jj + rr * T1;
+          if (j < XH)
+          {
+            const T *xr = xs + j * XW + i;
+            T vm = c0m[0] * xr[0], va = c0a[0] * xr[0];
+#pragma unroll
+            for (int o = 1; o < W; ++o)
+            {
+              vm = fma(c0m[o], xr[o], vm);
+              va = fma(c0a[o], xr[o], va);
+            }
+            zm[j * T0 + i] = vm;
+            za[j * T0 + i] = va;
+          }
+        }
+        if (it + 1 < NPL)
+          asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        // dir 1
+        T wm = T(0), ws = T(0);
+#pragma unroll
+        for (int o = 0; o < W; ++o)
+        {
+          const T vm = zm[(jj + o) * T0 + i], va = za[(jj + o) * T0 + i];
+          wm = fma(c1m[o], vm, wm);
+          ws = fma(c1a[o], vm, ws);
+          ws = fma(c1m[o], va, ws);
+        }
+        // dir 2: input plane q feeds output planes p = q - K + oo (oo = 0..2K)
+        // with coefficient band[res(p)][q - p + K] = band[res(p)][2K - oo];
+        // ring slot of output plane index (it - K + oo) is static (it = base + u)
+        const int rq = static_cast<int>(((q + 1) % K + K) % K);  // residue of plane q
+#pragma unroll
+        for (int oo = 0; oo < W; ++oo)
+        {
+          int res = rq + (oo % K);  // residue of output plane q - K + oo
+          if (res >= K)
+            res -= K;
+          const int slot = ((u - K + oo) % R + R) % R;
+          acc[slot] = fma(ba[res * W + (2 * K - oo)], wm, acc[slot]);
+          acc[slot] = fma(bm[res * W + (2 * K - oo)], ws, acc[slot]);
+        }
+        const int sl_out = ((u - K) % R + R) % R;
+        if (emit && out_ok)
+        {
+          const int64_t idx = (p_out * m + g1 + jj) * m + g0 + i;
+          if constexpr (RESID)
+            y[idx] = bval - acc[sl_out];
+          else
+            y[idx] = acc[sl_out];
+        }
+        acc[sl_out] = T(0);
       }
     }
-    if (++slot == R)
-      slot = 0;
   }
 }
 
@@ -151,8 +208,7 @@ __global__ void __launch_bounds__(128)
                       const T *__restrict__ b, T *__restrict__ y, int64_t m, int rchunk)
 {
   constexpr int T0 = 128, W = 2 * K + 1, R = 2 * K + 1, XW = T0 + 2 * K;
-  __shared__ T Xs[XW];
-  __shared__ T RM[R][T0], RA[R][T0];
+  __shared__ __align__(16) T Xs[2][XW];
   __shared__ T bm[K][W], ba[K][W];
   const int tid = threadIdx.x;
   for (int e = tid; e < K * W; e += T0)
@@ -164,62 +220,89 @@ __global__ void __launch_bounds__(128)
   const int64_t rs = static_cast<int64_t>(blockIdx.y) * rchunk;
   const int64_t re = min(rs + rchunk, m);
   const int i = tid;
-  const int res0 = static_cast<int>((g0 + i + 1) % K);
   __syncthreads();
   T c0m[W], c0a[W];
-#pragma unroll
-  for (int o = 0; o < W; ++o)
   {
-    c0m[o] = bm[res0][o];
-    c0a[o] = ba[res0][o];
-  }
-  int slot = 0;
-  for (int64_t q1 = rs - K; q1 < re + K; ++q1)
-  {
-    const bool rin = q1 >= 0 && q1 < m;
-    for (int e = tid; e < XW; e += T0)
-    {
-      const int64_t gx = g0 - K + e;
-      Xs[e] = (rin && gx >= 0 && gx < m) ? __ldg(x + q1 * m + gx) : T(0);
-    }
-    __syncthreads();
-    T zm = T(0), za = T(0);
+    const int res0 = static_cast<int>((g0 + i + 1) % K);
 #pragma unroll
     for (int o = 0; o < W; ++o)
     {
-      zm = fma(c0m[o], Xs[i + o], zm);
-      za = fma(c0a[o], Xs[i + o], za);
+      c0m[o] = bm[res0][o];
+      c0a[o] = ba[res0][o];
     }
-    RM[slot][i] = zm;
-    RA[slot][i] = za;
-    __syncthreads();
-    const int64_t g1 = q1 - K;
-    if (g1 >= rs)
+  }
+  auto load_row = [&](int64_t q, int buf) {
+    const bool rin = q >= 0 && q < m;
+    for (int e = tid; e < XW; e += T0)
     {
-      const int res1 = static_cast<int>((g1 + 1) % K);
-      T acc = T(0);
-      int s = slot + 1;
-      if (s == R)
-        s = 0;
+      const int64_t gx = g0 - K + e;
+      const bool ok = rin && gx >= 0 && gx < m;
+      op_cp_async(&Xs[buf][e], ok ? x + q * m + gx : x, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  const int NPL = static_cast<int>(re - rs) + 2 * K;
+  T acc[R];
 #pragma unroll
-      for (int o = 0; o < W; ++o)
+  for (int o = 0; o < R; ++o)
+    acc[o] = T(0);
+  load_row(rs - K, 0);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  for (int base = 0; base < NPL; base += R)
+  {
+#pragma unroll
+    for (int u = 0; u < R; ++u)
+    {
+      const int it = base + u;
+      if (it < NPL)
       {
-        acc = fma(ba[res1][o], RM[s][i], acc);
-        acc = fma(bm[res1][o], RA[s][i], acc);
-        if (++s == R)
-          s = 0;
-      }
-      if (g0 + i < m)
-      {
-        const int64_t idx = g1 * m + g0 + i;
+        const int buf = it & 1;
+        const int64_t q = rs - K + it;
+        if (it + 1 < NPL)
+          load_row(q + 1, buf ^ 1);
+        const int64_t p_out = q - K;
+        const bool emit = it >= 2 * K && p_out < re && g0 + i < m;
+        T bval = T(0);
         if constexpr (RESID)
-          y[idx] = __ldg(b + idx) - acc;
-        else
-          y[idx] = acc;
+        {
+          if (emit)
+            bval = __ldg(b + p_out * m + g0 + i);
+        }
+        T zm = T(0), za = T(0);
+#pragma unroll
+        for (int o = 0; o < W; ++o)
+        {
+          zm = fma(c0m[o], Xs[buf][i + o], zm);
+          za = fma(c0a[o], Xs[buf][i + o], za);
+        }
+        // 2D: y = A1 zM + M1 zA along direction 1
+        const int rq = static_cast<int>(((q + 1) % K + K) % K);
+#pragma unroll
+        for (int oo = 0; oo < W; ++oo)
+        {
+          int res = rq + (oo % K);
+          if (res >= K)
+            res -= K;
+          const int slot = ((u - K + oo) % R + R) % R;
+          acc[slot] = fma(ba[res][2 * K - oo], zm, acc[slot]);
+          acc[slot] = fma(bm[res][2 * K - oo], za, acc[slot]);
+        }
+        const int sl_out = ((u - K) % R + R) % R;
+        if (emit)
+        {
+          const int64_t idx = p_out * m + g0 + i;
+          if constexpr (RESID)
+            y[idx] = bval - acc[sl_out];
+          else
+            y[idx] = acc[sl_out];
+        }
+        acc[sl_out] = T(0);
+        if (it + 1 < NPL)
+          asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
       }
     }
-    if (++slot == R)
-      slot = 0;
   }
 }
 
@@ -233,8 +316,8 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
     constexpr size_t smem = op3d_smem<K, T>();
     const unsigned gx = static_cast<unsigned>((m + 31) / 32);
     const unsigned gy = static_cast<unsigned>((m + T1 - 1) / T1);
-    // z chunk: enough CTAs for ~4 waves over the SMs, but >= 2k planes
-    int64_t want = static_cast<int64_t>(sm_count) * 8;
+    // z chunk: enough CTAs for ~6 per SM, but >= 4k planes to bound the halo
+    int64_t want = static_cast<int64_t>(sm_count) * 6;
     int64_t nz = (want + gx * gy - 1) / (gx * gy);
     int64_t zchunk = (m + nz - 1) / nz;
     zchunk = std::max<int64_t>(zchunk, std::min<int64_t>(m, 4 * K));
@@ -242,9 +325,13 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
     auto kern = b ? level_op3d_kernel<K, T, true> : level_op3d_kernel<K, T, false>;
     static unsigned attr_mask[2] = {0, 0};
     if (first_on_device(attr_mask[b ? 1 : 0]))
+    {
       check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)),
                  "cudaFuncSetAttribute(level_op3d)");
+      check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                 "cudaFuncSetAttribute(level_op3d carveout)");
+    }
     kern<<<dim3(gx, gy, gz), 32 * T1, smem, s>>>(B, x, b, y, m, static_cast<int>(zchunk));
     check_launch("level_op3d_kernel");
   }
