@@ -36,7 +36,7 @@ constexpr size_t op3d_smem()
 {
   constexpr int T0 = 32, T1 = op_t1<K, T>(), W = 2 * K + 1;
   constexpr int XW = T0 + 2 * K, XH = T1 + 2 * K;
-  return sizeof(T) * (2 * static_cast<size_t>(XH) * XW + 4 * XH * T0 + 2 * K * W);
+  return sizeof(T) * (3 * static_cast<size_t>(XH) * XW + 3 * T1 * T0 + 4 * XH * T0 + 2 * K * W);
 }
 
 template <typename T>
@@ -60,8 +60,9 @@ __global__ void __launch_bounds__(32 * op_t1<K, T>())
   constexpr int XW = T0 + 2 * K, XH = T1 + 2 * K;
   constexpr int ROWS = (XH + T1 - 1) / T1;  // dir-0 rows per thread
   extern __shared__ __align__(16) unsigned char smraw[];
-  T *Xs = reinterpret_cast<T *>(smraw);  // [2][XH][XW]
-  T *ZM = Xs + 2 * XH * XW;              // [2][XH][T0]
+  T *Xs = reinterpret_cast<T *>(smraw);  // [3][XH][XW]  input planes (3-deep pipeline)
+  T *Bv = Xs + 3 * XH * XW;              // [3][T1][T0]  b of the output planes
+  T *ZM = Bv + 3 * T1 * T0;              // [2][XH][T0]
   T *ZA = ZM + 2 * XH * T0;              // [2][XH][T0]
   T *bm = ZA + 2 * XH * T0;              // [K][W]
   T *ba = bm + K * W;
@@ -92,11 +93,14 @@ __global__ void __launch_bounds__(32 * op_t1<K, T>())
     }
   }
   const bool out_ok = (g0 + i < m) && (g1 + jj < m);
+  const int NPL = static_cast<int>(ze - zs) + 2 * K;  // input planes zs-K .. ze+K-1
 
-  // x tile of input plane q (zero outside the domain) into buffer `buf`
-  auto load_plane = [&](int64_t q, int buf) {
+  // pipeline group `it`: input plane q = zs-K+it (x tile, zero outside) and,
+  // for the residual, b of the output plane emitted at iteration it (q - K)
+  auto issue = [&](int it) {
+    const int64_t q = zs - K + it;
     const bool zin = q >= 0 && q < m;
-    T *dst = Xs + buf * XH * XW;
+    T *dst = Xs + (it % 3) * XH * XW;
     for (int e = tid; e < XH * XW; e += NT)
     {
       const int jr = e / XW, ir = e - jr * XW;
@@ -104,17 +108,27 @@ __global__ void __launch_bounds__(32 * op_t1<K, T>())
       const bool ok = zin && gx >= 0 && gx < m && gy >= 0 && gy < m;
       op_cp_async(dst + e, ok ? x + (q * m + gy) * m + gx : x, ok);
     }
+    if constexpr (RESID)
+    {
+      const int64_t p = q - K;
+      const bool ok = out_ok && it >= 2 * K && p < ze;
+      op_cp_async(Bv + (it % 3) * NT + tid, ok ? b + (p * m + g1 + jj) * m + g0 + i : b, ok);
+    }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
-  const int NPL = static_cast<int>(ze - zs) + 2 * K;  // input planes zs-K .. ze+K-1
   T acc[R];
 #pragma unroll
   for (int o = 0; o < R; ++o)
     acc[o] = T(0);
 
-  load_plane(zs - K, 0);
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  issue(0);
+  if (NPL > 1)
+    issue(1);
+  if (NPL > 1)
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  else
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
 
   for (int base = 0; base < NPL; base += R)
@@ -125,23 +139,17 @@ __global__ void __launch_bounds__(32 * op_t1<K, T>())
       const int it = base + u;  // uniform across the CTA
       if (it < NPL)
       {
-        const int buf = it & 1;
+        const int bi = it % 3;
+        const int zb = it & 1;
         const int64_t q = zs - K + it;
-        if (it + 1 < NPL)
-          load_plane(q + 1, buf ^ 1);
-        // output plane emitted this iteration (inputs up to q are in)
+        if (it + 2 < NPL)
+          issue(it + 2);
         const int64_t p_out = q - K;
         const bool emit = it >= 2 * K && p_out < ze;
-        T bval = T(0);
-        if constexpr (RESID)
-        {
-          if (emit && out_ok)
-            bval = __ldg(b + (p_out * m + g1 + jj) * m + g0 + i);
-        }
         // dir 0: rows jj, jj+T1, ... of the tile
-        const T *xs = Xs + buf * XH * XW;
-        T *zm = ZM + buf * XH * T0;
-        T *za = ZA + buf * XH * T0;
+        const T *xs = Xs + bi * XH * XW;
+        T *zm = ZM + zb * XH * T0;
+        T *za = ZA + zb * XH * T0;
 #pragma unroll
         for (int rr = 0; rr < ROWS; ++rr)
         {
@@ -160,8 +168,11 @@ __global__ void __launch_bounds__(32 * op_t1<K, T>())
             za[j * T0 + i] = va;
           }
         }
-        if (it + 1 < NPL)
-          asm volatile("cp.async.wait_all;\n" ::: "memory");
+        // group it+1 complete (it+2 may stay in flight); all dir-0 rows visible
+        if (it + 2 < NPL)
+          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        else
+          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
         // dir 1
         T wm = T(0), ws = T(0);
@@ -175,7 +186,7 @@ __global__ void __launch_bounds__(32 * op_t1<K, T>())
         }
         // dir 2: input plane q feeds output planes p = q - K + oo (oo = 0..2K)
         // with coefficient band[res(p)][q - p + K] = band[res(p)][2K - oo];
-        // ring slot of output plane index (it - K + oo) is static (it = base + u)
+        // the ring slot of output plane index (it - K + oo) is static
         const int rq = static_cast<int>(((q + 1) % K + K) % K);  // residue of plane q
 #pragma unroll
         for (int oo = 0; oo < W; ++oo)
@@ -192,7 +203,7 @@ __global__ void __launch_bounds__(32 * op_t1<K, T>())
         {
           const int64_t idx = (p_out * m + g1 + jj) * m + g0 + i;
           if constexpr (RESID)
-            y[idx] = bval - acc[sl_out];
+            y[idx] = Bv[bi * NT + tid] - acc[sl_out];
           else
             y[idx] = acc[sl_out];
         }
