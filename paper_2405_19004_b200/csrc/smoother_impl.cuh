@@ -82,18 +82,41 @@ constexpr int sm_b_words()
 {
   return ipow(2 * K - 1, D) + 1;  // +1: odd patch stride
 }
-template <int D, int K>
+// Work-buffer layout of one patch: two arrays (zM | zA, later wMM | wS and
+// the residual / eigen-space tensor) with strides (1, S1, S2) over
+// [i0][j1][j2] (3D) or (1, S1) over [i0][j1] (2D), followed by ZPAD words.
+// S1 >= 2k-1, S2 >= (2k+1) S1; the paddings were chosen by an offline search
+// over the stage access patterns (bank-conflict model: 8-byte words hit bank
+// pair w mod 16, 4-byte words bank w mod 32) with a small memory penalty.
+template <int D, int K, typename T>
+struct ZLayout
+{
+  static constexpr bool F64 = sizeof(T) == 8;
+  static constexpr int t3d64[8][3] = {{0, 0, 0}, {1, 3, 7}, {3, 15, 3}, {5, 38, 5}, {7, 70, 5},
+                                      {9, 105, 11}, {11, 155, 0}, {13, 205, 0}};
+  static constexpr int t3d32[8][3] = {{0, 0, 0}, {1, 3, 3}, {3, 15, 0}, {5, 35, 15}, {7, 72, 1},
+                                      {9, 113, 3}, {11, 143, 0}, {13, 201, 0}};
+  static constexpr int t2d64[8][2] = {{0, 0}, {1, 1}, {3, 1}, {6, 1}, {10, 3}, {11, 7}, {11, 11}, {13, 7}};
+  static constexpr int t2d32[8][2] = {{0, 0}, {1, 1}, {3, 0}, {6, 17}, {9, 5}, {10, 13}, {12, 19}, {14, 9}};
+  static constexpr int S1 = D == 3 ? (F64 ? t3d64[K][0] : t3d32[K][0]) : (F64 ? t2d64[K][0] : t2d32[K][0]);
+  static constexpr int S2 = D == 3 ? (F64 ? t3d64[K][1] : t3d32[K][1]) : 0;
+  static constexpr int ZPAD = D == 3 ? (F64 ? t3d64[K][2] : t3d32[K][2]) : (F64 ? t2d64[K][1] : t2d32[K][1]);
+  static constexpr int ZS = D == 3 ? S2 * (2 * K + 1) : S1 * (2 * K + 1);  // one array
+  static constexpr int ZW = 2 * ZS + ZPAD;                                     // per patch
+  static_assert(S1 >= 2 * K - 1 && (D == 2 || S2 >= (2 * K + 1) * S1), "layout");
+};
+
+template <int D, int K, typename T>
 constexpr int sm_z_words()
 {
-  constexpr int NC = 2 * K + 1, NI = 2 * K - 1;
-  return 2 * ((D == 3) ? NI * NC * NC : NI * NC) + 1;
+  return ZLayout<D, K, T>::ZW;
 }
 
 template <int D, int K, typename T>
 constexpr size_t sm_smem_bytes()
 {
   return static_cast<size_t>(sm_pb<D, K, T>()) *
-         (sm_u_words<D, K>() + sm_b_words<D, K>() + sm_z_words<D, K>()) * sizeof(T);
+         (sm_u_words<D, K>() + sm_b_words<D, K>() + sm_z_words<D, K, T>()) * sizeof(T);
 }
 
 // ---------------------------------------------------------------------------
@@ -292,8 +315,9 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
   constexpr int PB = sm_pb<D, K, T>();
   constexpr int NT = sm_nt<D, K, T>();
   constexpr int NCD = ipow(NC, D), NID = ipow(NI, D);
-  constexpr int UW = sm_u_words<D, K>(), BW = sm_b_words<D, K>(), ZW = sm_z_words<D, K>();
-  constexpr int ZS = (ZW - 1) / 2;  // one work array (zM / wMM / r); the second follows
+  constexpr int UW = sm_u_words<D, K>(), BW = sm_b_words<D, K>();
+  using ZL = ZLayout<D, K, T>;
+  constexpr int ZW = ZL::ZW, ZS = ZL::ZS, S1 = ZL::S1, S2 = ZL::S2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *U = reinterpret_cast<T *>(smem_raw);  // [PB][UW]
   T *Bs = U + PB * UW;                     // [PB][BW]
@@ -429,7 +453,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
           T zm[NI], za[NI];
           eo_rows<K>(P.Me, P.Mo, ue, uo, zm);
           eo_rows<K>(P.Ae, P.Ao, ue, uo, za);
-          T *z = Z + p * ZW + NI * rr;  // strides (1, NI, NI*NC)
+          T *z = Z + p * ZW + S1 * (rr % NC) + S2 * (rr / NC);  // rr = j1 + NC j2
 #pragma unroll
           for (int i = 0; i < NI; ++i)
           {
@@ -450,13 +474,13 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
           const int p = tid / (NI * NC);
           const int rr = tid - p * (NI * NC);
           const int i0 = rr % NI, j2 = rr / NI;
-          T *z = Z + p * ZW + i0 + NI * NC * j2;
+          T *z = Z + p * ZW + i0 + S2 * j2;
           T zm[NC], za[NC];
 #pragma unroll
           for (int t = 0; t < NC; ++t)
           {
-            zm[t] = z[NI * t];
-            za[t] = z[ZS + NI * t];
+            zm[t] = z[S1 * t];
+            za[t] = z[ZS + S1 * t];
           }
           T zme[K + 1], zmo[K], zae[K + 1], zao[K];
           eo_split<NC>(zm, zme, zmo);
@@ -467,8 +491,8 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
 #pragma unroll
           for (int i = 0; i < NI; ++i)
           {
-            z[NI * i] = wm[i];
-            z[ZS + NI * i] = ws[i];
+            z[S1 * i] = wm[i];
+            z[ZS + S1 * i] = ws[i];
           }
         }
         __syncthreads();
@@ -483,7 +507,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
         const int gp = bt * PB + p;
         if (gp < a.total)
         {
-          T *z = Z + p * ZW + rr;
+          T *z = Z + p * ZW + i0 + S1 * i1;
           const T *bl = Bs + p * BW + rr;
           T r[NI];
           if constexpr (MODE == MODE_SOLVE)
@@ -498,8 +522,8 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
 #pragma unroll
             for (int t = 0; t < NC; ++t)
             {
-              wm[t] = z[NI * NC * t];
-              ws[t] = z[ZS + NI * NC * t];
+              wm[t] = z[S2 * t];
+              ws[t] = z[ZS + S2 * t];
             }
             T wme[K + 1], wmo[K], wse[K + 1], wso[K];
             eo_split<NC>(wm, wme, wmo);
@@ -525,7 +549,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
             eo_st<K>(P.Se, P.So, r, y);
 #pragma unroll
             for (int c = 0; c < NI; ++c)
-              z[NI * NC * c] = y[c];
+              z[S2 * c] = y[c];
           }
         }
       }
@@ -552,15 +576,15 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
         const int p = tid / (NI * NI);
         const int rr = tid - p * (NI * NI);
         const int i0 = rr % NI, i2 = rr / NI;
-        T *z = Z + p * ZW + i0 + NI * NC * i2;
+        T *z = Z + p * ZW + i0 + S2 * i2;
         T v[NI], y[NI];
 #pragma unroll
         for (int t = 0; t < NI; ++t)
-          v[t] = z[NI * t];
+          v[t] = z[S1 * t];
         eo_st<K>(P.Se, P.So, v, y);
 #pragma unroll
         for (int t = 0; t < NI; ++t)
-          z[NI * t] = y[t];
+          z[S1 * t] = y[t];
       }
       __syncthreads();
 
@@ -570,7 +594,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
         const int p = tid / (NI * NI);
         const int rr = tid - p * (NI * NI);
         const int i1 = rr % NI, i2 = rr / NI;
-        T *z = Z + p * ZW + NI * i1 + NI * NC * i2;
+        T *z = Z + p * ZW + S1 * i1 + S2 * i2;
         const T *inv = a.inv + NI * rr;
         T v[NI], y[NI];
 #pragma unroll
@@ -593,15 +617,15 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
         const int p = tid / (NI * NI);
         const int rr = tid - p * (NI * NI);
         const int i0 = rr % NI, i2 = rr / NI;
-        T *z = Z + p * ZW + i0 + NI * NC * i2;
+        T *z = Z + p * ZW + i0 + S2 * i2;
         T v[NI], y[NI];
 #pragma unroll
         for (int t = 0; t < NI; ++t)
-          v[t] = z[NI * t];
+          v[t] = z[S1 * t];
         eo_s<K>(P.Se, P.So, v, y);
 #pragma unroll
         for (int t = 0; t < NI; ++t)
-          z[NI * t] = y[t];
+          z[S1 * t] = y[t];
       }
       __syncthreads();
 
@@ -616,11 +640,11 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
         {
           int64_t g0, g1, g2;
           origin(cur, p, g0, g1, g2);
-          const T *z = Z + p * ZW + rr;
+          const T *z = Z + p * ZW + i0 + S1 * i1;
           T v[NI], y[NI];
 #pragma unroll
           for (int t = 0; t < NI; ++t)
-            v[t] = z[NI * NC * t];
+            v[t] = z[S2 * t];
           eo_s<K>(P.Se, P.So, v, y);
           T *xp = a.x + ((g2 + 1 - a.zoff) * m + (g1 + 1 + i1)) * m + (g0 + 1 + i0);
           // x^I old values are still in the staged closure (no other patch of
@@ -659,7 +683,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
           T zm[NI], za[NI];
           eo_rows<K>(P.Me, P.Mo, ue, uo, zm);
           eo_rows<K>(P.Ae, P.Ao, ue, uo, za);
-          T *z = Z + p * ZW + NI * j1;
+          T *z = Z + p * ZW + S1 * j1;
 #pragma unroll
           for (int i = 0; i < NI; ++i)
           {
@@ -698,8 +722,8 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
 #pragma unroll
             for (int t = 0; t < NC; ++t)
             {
-              zm[t] = z[NI * t];
-              za[t] = z[ZS + NI * t];
+              zm[t] = z[S1 * t];
+              za[t] = z[ZS + S1 * t];
             }
             T zme[K + 1], zmo[K], zae[K + 1], zao[K];
             eo_split<NC>(zm, zme, zmo);
@@ -725,7 +749,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
             eo_st<K>(P.Se, P.So, r, y);
 #pragma unroll
             for (int c = 0; c < NI; ++c)
-              z[NI * c] = y[c];
+              z[S1 * c] = y[c];
           }
         }
       }
@@ -743,7 +767,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
       {
         const int p = tid / NI;
         const int i1 = tid - p * NI;
-        T *z = Z + p * ZW + NI * i1;
+        T *z = Z + p * ZW + S1 * i1;
         const T *inv = a.inv + NI * i1;
         T v[NI], y[NI];
 #pragma unroll
@@ -774,7 +798,7 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
           T v[NI], y[NI];
 #pragma unroll
           for (int t = 0; t < NI; ++t)
-            v[t] = z[NI * t];
+            v[t] = z[S1 * t];
           eo_s<K>(P.Se, P.So, v, y);
           T *xp = a.x + (g1 + 1) * m + (g0 + 1 + i0);
           const T *xo = U + p * UW + (1 + i0) + NC;
