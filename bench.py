@@ -349,12 +349,16 @@ def main():
         try:
             s = json.load(open(NCU_SUMMARY))
             key = f"d{args.dim}k{args.degree}L{args.level}{args.dtype}{args.variant}"
-            traffic = s.get(key, {}).get("dram_bytes_per_step")
+            per = s.get(key, {}).get("dram_bytes_per_launch")
+            if per:  # ncu captured colour launch(es), cold L2: scale to the 2^d launches of a step
+                traffic = float(np.mean(per)) * sum(1 for c in colour_patch_counts if c)
         except Exception:
             traffic = None
     roofline = {
         "bound": "hbm", "achieved": alg_bytes / launch_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
         "frac": alg_bytes / launch_s / 1e9 / hbm_peak, "traffic": traffic,
+        "traffic_note": "DRAM read+write bytes per step from ncu --set full (profiles/ncu_summary.json; "
+                        "cold L2, per-colour launch x colours)",
         "kernel": "vp_smooth_kernel (one launch per colour, summed over the 2^d colours)",
         "algorithmic_bytes_per_step": alg_bytes,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
