@@ -180,6 +180,14 @@ int pmg_host_level_setup(int dim, int degree, int level, double *S, double *lamb
 /* Number of kernel launches issued by this library since load (counter). */
 int64_t pmg_launch_count(void);
 
+/* Smoother kernel organisation for subsequent calls (process-wide; no
+ * reference counterpart, the reference has one CPU loop): 0 = per-degree
+ * default, 1 = line-per-thread kernel everywhere, 2 = plane-streaming kernel
+ * where it exists (3D, degree <= 3, fused / boundary). Results agree to
+ * rounding; used for A/B measurement. Returns PMG_ERR_INVALID otherwise. */
+int pmg_set_smoother_impl(int impl);
+int pmg_get_smoother_impl(void);
+
 #ifdef __cplusplus
 }
 #endif

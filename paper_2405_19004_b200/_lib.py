@@ -56,6 +56,8 @@ SIGNATURES = [
     ("pmg_level_setup_data", _i, [_vp, _pd, _pd, _pd, _pd, _pd, _pd, _pd]),
     ("pmg_host_level_setup", _i, [_i, _i, _i] + [_pd] * 9 + [_pi]),
     ("pmg_launch_count", _i64, []),
+    ("pmg_set_smoother_impl", _i, [_i]),
+    ("pmg_get_smoother_impl", _i, []),
 ]
 
 _lib = None

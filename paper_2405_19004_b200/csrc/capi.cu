@@ -32,6 +32,9 @@ thread_local std::string g_last_error;
 
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+std::atomic<int> g_smoother_impl{SMOOTHER_IMPL_AUTO};
+int smoother_impl_choice() { return g_smoother_impl.load(std::memory_order_relaxed); }
+
 void check_launch(const char *what)
 {
   check_cuda(cudaGetLastError(), what);
@@ -186,6 +189,27 @@ void level_init(pmg_level_s *l)
   const auto &S = l->S;
   {
     std::vector<T> v(S.eo_mats.begin(), S.eo_mats.end());
+    if (S.k == 1)
+    {
+      // PointStencil<T> after PatchMatsEO<T,1> (smoother_point.cuh): the 3^d
+      // interior row of A-bar = sum over directions of A in one, M in the others
+      // (fastdiag.cpp:211-232), and coef = S^(2d) / sum(lambda) (fastdiag.cpp:164-192)
+      const double Mr[3] = {S.mass_if(0, 0), S.mass_if(0, 1), S.mass_if(0, 2)};
+      const double Ar[3] = {S.stiff_if(0, 0), S.stiff_if(0, 1), S.stiff_if(0, 2)};
+      double w[27] = {0};
+      for (int t2 = 0; t2 < (S.dim == 3 ? 3 : 1); ++t2)
+        for (int t1 = 0; t1 < 3; ++t1)
+          for (int t0 = 0; t0 < 3; ++t0)
+            w[9 * t2 + 3 * t1 + t0] =
+                S.dim == 3 ? Ar[t0] * Mr[t1] * Mr[t2] + Mr[t0] * Ar[t1] * Mr[t2] + Mr[t0] * Mr[t1] * Ar[t2]
+                           : Ar[t0] * Mr[t1] + Mr[t0] * Ar[t1];
+      const double s = S.S(0, 0);
+      double coef = S.inv_sums[0];
+      for (int d = 0; d < 2 * S.dim; ++d)
+        coef *= s;
+      v.insert(v.end(), w, w + 27);
+      v.push_back(static_cast<T>(coef));
+    }
     l->patch_mats.resize(v.size() * sizeof(T));
     std::memcpy(l->patch_mats.data(), v.data(), l->patch_mats.size());
   }
@@ -617,6 +641,19 @@ const char *pmg_last_error(void) { return g_last_error.c_str(); }
 int pmg_version(void) { return 1; }
 
 int64_t pmg_launch_count(void) { return g_launches.load(); }
+
+int pmg_set_smoother_impl(int impl)
+{
+  if (impl < SMOOTHER_IMPL_AUTO || impl > SMOOTHER_IMPL_PLANE)
+  {
+    g_last_error = "pmg_set_smoother_impl: impl must be 0, 1 or 2";
+    return PMG_ERR_INVALID;
+  }
+  g_smoother_impl.store(impl);
+  return PMG_OK;
+}
+
+int pmg_get_smoother_impl(void) { return g_smoother_impl.load(); }
 
 int pmg_device_info(int device, int *sm_count, int *sm_clock_khz, int *cc_major, int *cc_minor)
 {

@@ -26,6 +26,16 @@ inline void check_cuda(cudaError_t e, const char *what)
 }
 
 void note_launch(int n = 1);       // counts kernel launches (pmg_launch_count)
+
+// smoother kernel organisation (pmg_set_smoother_impl): 0 = per-degree default,
+// 1 = line kernel everywhere, 2 = plane-streaming kernel where it exists
+enum : int
+{
+  SMOOTHER_IMPL_AUTO = 0,
+  SMOOTHER_IMPL_LINE = 1,
+  SMOOTHER_IMPL_PLANE = 2
+};
+int smoother_impl_choice();
 void check_launch(const char *what);  // cudaGetLastError + count
 
 // true the first time it is called for the current device with this mask

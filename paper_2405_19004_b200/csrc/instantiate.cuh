@@ -5,6 +5,8 @@
 #include "dispatch.hpp"
 #include "operator_impl.cuh"
 #include "smoother_impl.cuh"
+#include "smoother_plane.cuh"
+#include "smoother_point.cuh"
 #include "transfer_impl.cuh"
 
 #define PMG_CAT2(a, b) a##b
@@ -15,10 +17,44 @@ namespace pmgb
 namespace
 {
 
+// 3D fused / boundary sweeps of degree <= PMG_PLANE_KMAX use the plane-streaming
+// kernel (smoother_plane.cuh) unless pmg_set_smoother_impl selects the line one
+#ifndef PMG_PLANE_KMAX
+#define PMG_PLANE_KMAX 2
+#endif
+
 template <int D, typename T>
 void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, cudaStream_t s)
 {
-  launch_vp_smooth_mode<D, PMG_K, T>(*static_cast<const PatchMatsEO<T, PMG_K> *>(P), a, mode, sm_count, s);
+  const auto &PM = *static_cast<const PatchMatsEO<T, PMG_K> *>(P);
+  const int impl = smoother_impl_choice();
+  if constexpr (PMG_K == 1)
+  {
+    // degree 1: point-stencil kernel (smoother_point.cuh); the stencil follows
+    // the even-odd matrices in the level's parameter blob (capi.cu level_init)
+    if (impl == SMOOTHER_IMPL_AUTO && (mode == MODE_FUSED || mode == MODE_BOUNDARY))
+    {
+      const auto &st = *reinterpret_cast<const PointStencil<T> *>(static_cast<const unsigned char *>(P) +
+                                                                   sizeof(PatchMatsEO<T, 1>));
+      if (mode == MODE_FUSED)
+        launch_vp_point<D, T, MODE_FUSED>(st, a, s);
+      else
+        launch_vp_point<D, T, MODE_BOUNDARY>(st, a, s);
+      return;
+    }
+  }
+  if constexpr (D == 3 && PMG_K <= PMG_PLANE_KMAX)
+  {
+    if (impl != SMOOTHER_IMPL_LINE && (mode == MODE_FUSED || mode == MODE_BOUNDARY))
+    {
+      if (mode == MODE_FUSED)
+        launch_vp_smooth_plane<PMG_K, T, MODE_FUSED>(PM, a, s);
+      else
+        launch_vp_smooth_plane<PMG_K, T, MODE_BOUNDARY>(PM, a, s);
+      return;
+    }
+  }
+  launch_vp_smooth_mode<D, PMG_K, T>(PM, a, mode, sm_count, s);
 }
 
 template <int D, typename T>

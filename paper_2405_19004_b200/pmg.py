@@ -36,8 +36,25 @@ __all__ = [
     "MultigridContext", "make_multigrid_context", "SmootherVariant", "smooth", "smooth_color", "smooth_color_slab",
     "apply_laplacian", "compute_residual", "prolongate", "restrict_vector", "v_cycle",
     "full_multigrid", "FmgStats", "vector_norm", "compute_rhs", "l2_error", "gmres", "SolveStats",
-    "DivergenceError",
+    "DivergenceError", "set_smoother_impl", "get_smoother_impl",
 ]
+
+_SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2}
+
+
+def set_smoother_impl(impl: str = "auto") -> None:
+    """Select the smoother kernel organisation for later calls (A/B
+    measurement; no reference counterpart): "auto" (per-degree default),
+    "line" (line-per-thread kernel) or "plane" (plane-streaming kernel, 3D
+    fused/boundary, degree <= 3)."""
+    if impl not in _SMOOTHER_IMPLS:
+        raise ValueError(f"smoother impl must be one of {sorted(_SMOOTHER_IMPLS)}")
+    check(_lib.load().pmg_set_smoother_impl(_SMOOTHER_IMPLS[impl]), "set_smoother_impl")
+
+
+def get_smoother_impl() -> str:
+    code = _lib.load().pmg_get_smoother_impl()
+    return {v: k for k, v in _SMOOTHER_IMPLS.items()}[code]
 
 
 class SmootherVariant:

@@ -175,3 +175,18 @@ def test_no_cpu_fallback_without_gpu(lib):
         pmg.make_level_context(pmg.CartesianLevel(2, 3, 2))
     h = ctypes.c_void_p()
     assert lib.pmg_mg_create(3, 2, 2, 0, 2, 0, ctypes.byref(h)) in (2, 4)
+
+
+def test_smoother_impl_switch(lib):
+    import paper_2405_19004_b200 as pmg
+
+    assert lib.pmg_set_smoother_impl(7) != 0
+    assert lib.pmg_set_smoother_impl(-1) != 0
+    try:
+        for name in ["line", "plane", "auto"]:
+            pmg.set_smoother_impl(name)
+            assert pmg.get_smoother_impl() == name
+        with pytest.raises(ValueError):
+            pmg.set_smoother_impl("tensor")
+    finally:
+        pmg.set_smoother_impl("auto")

@@ -250,3 +250,28 @@ def test_cpp_shim(pmg, cuda):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "OK" in out.stdout
+
+
+# Both kernel organisations of the 3D low-degree smoother (line-per-thread and
+# plane-streaming) against the reference, including levels whose colour sizes
+# are not multiples of the patches-per-CTA (ragged last CTA) and level 1
+# (a single patch, the coarse solve).
+@pytest.mark.parametrize("impl", ["auto", "line", "plane"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", [(2, 1, 1), (2, 1, 6), (3, 1, 1), (3, 1, 5), (3, 2, 1), (3, 2, 3), (3, 2, 5), (3, 3, 1), (3, 3, 4)],
+                         ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")
+def test_smoother_impls(pmg, cuda, case, dtype, impl):
+    dim, k, L = case
+    ref = refbind.RefMg(dim, k, L, prec=0 if dtype == np.float64 else 1)
+    ctx = pmg.make_multigrid_context(dim, k, L, dtype=dtype)
+    lev = ctx.levels[-1]
+    x0, b = inputs(lev.level.total_dofs, dtype, seed=7)
+    pmg.set_smoother_impl(impl)
+    try:
+        for variant in ["fused", "boundary"]:
+            xd = dev(cuda, x0.copy())
+            pmg.smooth(lev, xd, dev(cuda, b), variant)
+            want = ref.smooth(L - 1, x0, b, variant)
+            assert rel(xd.cpu().numpy(), want) < TOL[dtype], (variant, rel(xd.cpu().numpy(), want))
+    finally:
+        pmg.set_smoother_impl("auto")

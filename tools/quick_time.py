@@ -69,5 +69,9 @@ if __name__ == "__main__":
     else:
         cfgs = [(int(args[i]), int(args[i + 1]), int(args[i + 2]), args[i + 3], args[i + 4])
                 for i in range(0, len(args), 5)]
+    impls = os.environ.get("PMG_IMPLS", "auto").split(",")
     for c in cfgs:
-        run(*c)
+        for impl in impls:
+            pmg.set_smoother_impl(impl)
+            print(f"[{impl}] ", end="")
+            run(*c)
