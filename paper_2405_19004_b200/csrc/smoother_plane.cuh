@@ -36,100 +36,103 @@ struct PlaneCfg
 {
   static constexpr int NC = 2 * K + 1, NI = 2 * K - 1;
   static constexpr bool F64 = sizeof(T) == 8;
-  // patches per CTA
-  static constexpr int PB = K == 1 ? 64 : (K == 2 ? 16 : 8);
+  // patches per CTA: PB consecutive patches of one x-row of the colour
+  static constexpr int PB = K == 1 ? 64 : 16;
   // threads: the widest phase (P1: NC per patch, P2/P4: NI^2 per patch)
   static constexpr int LANES = (NC > NI * NI ? NC : NI * NI);
   static constexpr int NT = ((PB * LANES + 31) / 32) * 32;
-  static constexpr int UW = NC * NC * NC;  // odd: plane reads are conflict-free
-  // W stride per patch (words): 2 NC NI^2 + pad (tools/bank_search.py)
-  static constexpr int WPAD64[4] = {0, 1, 3, 1};
-  static constexpr int WPAD32[4] = {0, 1, 3, 1};
-  static constexpr int WW = 2 * NC * NI * NI + (F64 ? WPAD64[K] : WPAD32[K]);
+  static constexpr int RX = 2 * K * PB + 1;  // x extent of the CTA's closure union
+  // shared-memory layout (words), tools/bank_search.py:
+  //   U[p][t2][t1][t0] at p UW + t2 SU2 + t1 SU1 + t0
+  //   W: wMM[j][q] at p WW + j SJ + q, wS at p WW + SW + j SJ + q (q = i0 + NI i1);
+  //      the eigen-space tensor overwrites wMM in place
+  static constexpr int L64[4][6] = {{0}, {57, 5, 19, 19, 1, 3}, {135, 5, 27, 105, 10, 50}, {0}};
+  static constexpr int L32[4][6] = {{0}, {39, 3, 13, 41, 3, 16}, {145, 5, 29, 105, 10, 50}, {0}};
+  static constexpr int UW = F64 ? L64[K][0] : L32[K][0];
+  static constexpr int SU1 = F64 ? L64[K][1] : L32[K][1];
+  static constexpr int SU2 = F64 ? L64[K][2] : L32[K][2];
+  static constexpr int WW = F64 ? L64[K][3] : L32[K][3];
+  static constexpr int SJ = F64 ? L64[K][4] : L32[K][4];
+  static constexpr int SW = F64 ? L64[K][5] : L32[K][5];
+  static_assert(SU1 >= NC && SU2 >= NC * SU1 && UW >= NC * SU2, "U layout");
+  static_assert(SJ >= NI * NI && SW >= NC * SJ && WW >= SW + NC * SJ, "W layout");
   static constexpr size_t SMEM = static_cast<size_t>(PB) * (UW + WW) * sizeof(T);
 };
 
+// grid = (ceil(np0 / PB), np1, np2): CTA (bx, j1, j2) owns patches
+// j0 = bx PB + p of the colour, so the closures of its patches form one
+// contiguous box of x rows and the global -> shared copy runs along x.
 template <int K, typename T, int MODE>
 __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
     vp_smooth_plane_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ ColorArgs<T> a)
 {
   using C = PlaneCfg<K, T>;
-  constexpr int NC = C::NC, NI = C::NI, PB = C::PB, NT = C::NT, UW = C::UW, WW = C::WW;
-  constexpr int NI2 = NI * NI, NC2 = NC * NC;
+  constexpr int NC = C::NC, NI = C::NI, PB = C::PB, NT = C::NT, RX = C::RX;
+  constexpr int UW = C::UW, SU1 = C::SU1, SU2 = C::SU2, WW = C::WW, SJ = C::SJ, SW = C::SW;
+  constexpr int NI2 = NI * NI;
   constexpr int HO = K > 1 ? K - 1 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *U = reinterpret_cast<T *>(smem_raw);  // [PB][UW]  closure, [t2][t1][t0]
+  T *U = reinterpret_cast<T *>(smem_raw);  // [PB][UW]  closures
   T *W = U + PB * UW;                      // [PB][WW]  work
-  __shared__ int org[PB][3];
 
   const int tid = threadIdx.x;
   const int64_t m = a.m;
   const int64_t m2 = m * m;
-  const int p0 = blockIdx.x * PB;
+  const int npv = min(PB, a.np[0] - static_cast<int>(blockIdx.x) * PB);  // valid patches
+  // closure-local t = 0 per direction: g_a = k (v_a - 1) - 1, v_a = 2 j_a + vb_a
+  // (patches.cpp:71); patch p of the CTA starts at G0 + 2K p along x
+  const int G0 = K * (2 * static_cast<int>(blockIdx.x) * PB + a.vb[0] - 1) - 1;
+  const int G1 = K * (2 * static_cast<int>(blockIdx.y) + a.vb[1] - 1) - 1;
+  const int64_t G2g = static_cast<int64_t>(K) * (2 * static_cast<int64_t>(blockIdx.z) + a.vb[2] - 1) - 1;
+  const int64_t G2 = G2g - a.zoff;  // local plane of t2 = 0 in x / b
 
-  if (tid < PB)
+  // ---- stage the closures of x, zero-filled outside the domain (gather,
+  //      patches.cpp:72-79). Thread -> union column (X, t1), then a fixed-stride
+  //      walk over the NC planes t2; lanes run along contiguous x. Column X
+  //      belongs to patch X / 2K (t0 = X mod 2K) and, on a shared vertex column,
+  //      also to patch X / 2K - 1 (t0 = 2K). ------------------------------------
+#pragma unroll 1
+  for (int line = tid; line < NC * RX; line += NT)
   {
-    const int gp = p0 + tid;
-    int g0 = -(1 << 30), g1 = -(1 << 30), g2 = -(1 << 30);  // invalid patch: every load masked
-    if (gp < a.total)
-    {
-      const int j0 = gp % a.np[0];
-      const int rest = gp / a.np[0];
-      const int j1 = rest % a.np[1];
-      const int j2 = rest / a.np[1];
-      // closure-local t = 0 per direction: g_a = k (v_a - 1) - 1 (patches.cpp:71)
-      g0 = K * (2 * j0 + a.vb[0] - 1) - 1;
-      g1 = K * (2 * j1 + a.vb[1] - 1) - 1;
-      g2 = K * (2 * j2 + a.vb[2] - 1) - 1 - static_cast<int>(a.zoff);
-    }
-    org[tid][0] = g0;
-    org[tid][1] = g1;
-    org[tid][2] = g2;
-  }
-  __syncthreads();
-
-  // ---- stage the closure of x: one z-line (NC elements) per thread-iteration,
-  //      zero-filled outside the domain (gather, patches.cpp:72-79) ----------
-  {
-    for (int line = tid; line < PB * NC2; line += NT)
-    {
-      const int p = line / NC2;
-      const int rr = line - p * NC2;
-      const int t0 = rr % NC, t1 = rr / NC;
-      const int y0 = org[p][0] + t0, y1 = org[p][1] + t1, z0 = org[p][2];
-      const bool inplane = static_cast<uint32_t>(y0) < static_cast<uint32_t>(m) &&
-                           static_cast<uint32_t>(y1) < static_cast<uint32_t>(m);
-      const T *src = a.x + static_cast<int64_t>(y1) * m + y0;
-      T *dst = U + p * UW + rr;
+    const int t1 = line / RX;
+    const int X = line - t1 * RX;
+    const int gx = G0 + X, gy = G1 + t1;
+    const bool okxy = static_cast<unsigned>(gx) < static_cast<unsigned>(m) &&
+                      static_cast<unsigned>(gy) < static_cast<unsigned>(m);
+    const int pq = X / (2 * K);
+    const int p = pq < PB ? pq : PB - 1;
+    const int t0 = X - 2 * K * p;
+    const bool dup = t0 == 0 && p > 0;
+    T *dst = U + p * UW + t1 * SU1 + t0;
+    T *dst2 = U + (p - 1) * UW + t1 * SU1 + 2 * K;
+    const T *src = a.x + G2 * m2 + static_cast<int64_t>(gy) * m + gx;
 #pragma unroll
-      for (int t = 0; t < NC; ++t)
-      {
-        const int64_t zl = static_cast<int64_t>(z0) + t;  // local plane; global = zl + zoff
-        bool ok = inplane && static_cast<uint64_t>(zl + a.zoff) < static_cast<uint64_t>(a.mz);
-        if constexpr (MODE == MODE_BOUNDARY)
-        {
-          const bool inner = t0 >= 1 && t0 <= NC - 2 && t1 >= 1 && t1 <= NC - 2 && t >= 1 && t <= NC - 2;
-          ok = ok && !inner;
-        }
-        cp_async_elem(dst + NC2 * t, ok ? src + zl * m2 : a.x, ok);
-      }
+    for (int t2 = 0; t2 < NC; ++t2)
+    {
+      const bool ok = okxy && static_cast<uint64_t>(G2g + t2) < static_cast<uint64_t>(a.mz);
+      bool ok1 = ok;
+      if constexpr (MODE == MODE_BOUNDARY)  // never reads x^I (smoother.cpp:128-148)
+        ok1 = ok && !(t0 >= 1 && t0 <= NC - 2 && t1 >= 1 && t1 <= NC - 2 && t2 >= 1 && t2 <= NC - 2);
+      const T *sp = ok ? src + t2 * m2 : a.x;
+      cp_async_elem(dst + t2 * SU2, sp, ok1);
+      if (dup)
+        cp_async_elem(dst2 + t2 * SU2, sp, ok);
     }
-    cp_async_commit();
   }
+  cp_async_commit();
 
   // ---- b^I of this thread's (p, i0, i1) column, straight into registers ------
   const int p24 = tid / NI2;
   const int rr24 = tid - p24 * NI2;
   const int i0_24 = rr24 % NI, i1_24 = rr24 / NI;
-  const bool act24 = tid < PB * NI2 && p0 + p24 < a.total;
+  const bool act24 = tid < PB * NI2 && p24 < npv;
+  const int64_t col24 = (G2 + 1) * m2 + static_cast<int64_t>(G1 + 1 + i1_24) * m + (G0 + 2 * K * p24 + 1 + i0_24);
   T bcol[NI];
   if (act24)
   {
-    const T *bp = a.b + (static_cast<int64_t>(org[p24][2]) + 1) * m2 +
-                  static_cast<int64_t>(org[p24][1] + 1 + i1_24) * m + (org[p24][0] + 1 + i0_24);
 #pragma unroll
     for (int i = 0; i < NI; ++i)
-      bcol[i] = __ldg(bp + i * m2);
+      bcol[i] = __ldg(a.b + col24 + i * m2);
   }
 
   cp_async_wait_all();
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
   {
     const int p = tid / NC;
     const int j2 = tid - p * NC;
-    const T *up = U + p * UW + j2 * NC2;
+    const T *up = U + p * UW + j2 * SU2;
     // even / odd accumulators of wMM = M1 zM and wS = A1 zM + M1 zA over j1
     T Em[K][NI], Es[K][NI], Om[HO][NI], Os[HO][NI];
 #pragma unroll
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
       T zma[NI], zaa[NI];
 #pragma unroll
       for (int t = 0; t < NC; ++t)
-        ra[t] = up[jj * NC + t];
+        ra[t] = up[jj * SU1 + t];
       eo_split<NC>(ra, rae, rao);
       eo_rows<K>(P.Me, P.Mo, rae, rao, zma);
       eo_rows<K>(P.Ae, P.Ao, rae, rao, zaa);
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
         T zmb[NI], zab[NI];
 #pragma unroll
         for (int t = 0; t < NC; ++t)
-          rb[t] = up[(NC - 1 - jj) * NC + t];
+          rb[t] = up[(NC - 1 - jj) * SU1 + t];
         eo_split<NC>(rb, rbe, rbo);
         eo_rows<K>(P.Me, P.Mo, rbe, rbo, zmb);
         eo_rows<K>(P.Ae, P.Ao, rbe, rbo, zab);
@@ -174,13 +177,13 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
           {
             if (jj == 0)
             {
-              Em[h][i] = (P.Me[h][jj]) * zme;
-              Es[h][i] = fma((P.Ae[h][jj]), zme, (P.Me[h][jj]) * zae);
+              Em[h][i] = P.Me[h][jj] * zme;
+              Es[h][i] = fma(P.Ae[h][jj], zme, P.Me[h][jj] * zae);
             }
             else
             {
-              Em[h][i] = fma((P.Me[h][jj]), zme, Em[h][i]);
-              Es[h][i] = fma((P.Ae[h][jj]), zme, fma((P.Me[h][jj]), zae, Es[h][i]));
+              Em[h][i] = fma(P.Me[h][jj], zme, Em[h][i]);
+              Es[h][i] = fma(P.Ae[h][jj], zme, fma(P.Me[h][jj], zae, Es[h][i]));
             }
           }
 #pragma unroll
@@ -188,13 +191,13 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
           {
             if (jj == 0)
             {
-              Om[h][i] = (P.Mo[h][jj]) * zmo;
-              Os[h][i] = fma((P.Ao[h][jj]), zmo, (P.Mo[h][jj]) * zao);
+              Om[h][i] = P.Mo[h][jj] * zmo;
+              Os[h][i] = fma(P.Ao[h][jj], zmo, P.Mo[h][jj] * zao);
             }
             else
             {
-              Om[h][i] = fma((P.Mo[h][jj]), zmo, Om[h][i]);
-              Os[h][i] = fma((P.Ao[h][jj]), zmo, fma((P.Mo[h][jj]), zao, Os[h][i]));
+              Om[h][i] = fma(P.Mo[h][jj], zmo, Om[h][i]);
+              Os[h][i] = fma(P.Ao[h][jj], zmo, fma(P.Mo[h][jj], zao, Os[h][i]));
             }
           }
         }
@@ -213,8 +216,8 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
         }
       }
     }
-    // W[p]: wMM at [j2][i1][i0], wS at NC NI^2 + [j2][i1][i0]
-    T *wp = W + p * WW + j2 * NI2;
+    // wMM[j2][i1][i0], wS[j2][i1][i0]
+    T *wp = W + p * WW + j2 * SJ;
 #pragma unroll
     for (int h = 0; h < K; ++h)
     {
@@ -225,13 +228,13 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
         {
           wp[h * NI + i] = Em[h][i] + Om[h][i];
           wp[(NI - 1 - h) * NI + i] = Em[h][i] - Om[h][i];
-          wp[NC * NI2 + h * NI + i] = Es[h][i] + Os[h][i];
-          wp[NC * NI2 + (NI - 1 - h) * NI + i] = Es[h][i] - Os[h][i];
+          wp[SW + h * NI + i] = Es[h][i] + Os[h][i];
+          wp[SW + (NI - 1 - h) * NI + i] = Es[h][i] - Os[h][i];
         }
         else
         {
           wp[h * NI + i] = Em[h][i];
-          wp[NC * NI2 + h * NI + i] = Es[h][i];
+          wp[SW + h * NI + i] = Es[h][i];
         }
       }
     }
@@ -246,8 +249,8 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
 #pragma unroll
     for (int t = 0; t < NC; ++t)
     {
-      wm[t] = wl[t * NI2];
-      ws[t] = wl[NC * NI2 + t * NI2];
+      wm[t] = wl[t * SJ];
+      ws[t] = wl[SW + t * SJ];
     }
     T wme[K + 1], wmo[K], wse[K + 1], wso[K];
     eo_split<NC>(wm, wme, wmo);
@@ -260,16 +263,16 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
     eo_st<K>(P.Se, P.So, r, y);
 #pragma unroll
     for (int c = 0; c < NI; ++c)
-      wl[c * NI2] = y[c];
+      wl[c * SJ] = y[c];
   }
   __syncthreads();
 
   // ---- P3: thread (p, c2): eigen plane c2 in registers ----------------------------
-  if (tid < PB * NI)
+  if (tid < PB * NI && tid / NI < npv)
   {
     const int p = tid / NI;
     const int c2 = tid - p * NI;
-    T *wq = W + p * WW + c2 * NI2;
+    T *wq = W + p * WW + c2 * SJ;
     T v[NI][NI];  // [i1][i0] -> [c1][c0] -> back
 #pragma unroll
     for (int i1 = 0; i1 < NI; ++i1)
@@ -324,18 +327,17 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
     T yh[NI], v[NI];
 #pragma unroll
     for (int c = 0; c < NI; ++c)
-      yh[c] = wl[c * NI2];
+      yh[c] = wl[c * SJ];
     eo_s<K>(P.Se, P.So, yh, v);
-    T *xp = a.x + (static_cast<int64_t>(org[p24][2]) + 1) * m2 +
-            static_cast<int64_t>(org[p24][1] + 1 + i1_24) * m + (org[p24][0] + 1 + i0_24);
-    const T *xo = U + p24 * UW + (1 + i0_24) + NC * (1 + i1_24) + NC2;
+    T *xp = a.x + col24;
+    const T *xo = U + p24 * UW + SU2 + (1 + i1_24) * SU1 + (1 + i0_24);
 #pragma unroll
     for (int i = 0; i < NI; ++i)
     {
       if constexpr (MODE == MODE_BOUNDARY)
         xp[i * m2] = v[i];
       else
-        xp[i * m2] = xo[NC2 * i] + v[i];  // x^I_old is in the staged closure
+        xp[i * m2] = xo[SU2 * i] + v[i];  // x^I_old is in the staged closure
     }
   }
 }
@@ -354,9 +356,9 @@ void launch_vp_smooth_plane(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a, c
                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100),
                "cudaFuncSetAttribute(plane smoother carveout)");
   }
-  const int grid = (a.total + C::PB - 1) / C::PB;
-  if (grid == 0)
+  if (a.total == 0)
     return;
+  const dim3 grid((a.np[0] + C::PB - 1) / C::PB, a.np[1], a.np[2]);
   vp_smooth_plane_kernel<K, T, MODE><<<grid, C::NT, C::SMEM, s>>>(P, a);
   check_launch("vp_smooth_plane_kernel");
 }
