@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpmg_b200.so")
+# PMG_B200_LIB: an alternative in-tree build (A/B experiments of kernel variants)
+LIB_PATH = os.environ.get("PMG_B200_LIB") or os.path.join(_HERE, "libpmg_b200.so")
 
 PMG_OK, PMG_ERR_INVALID, PMG_ERR_RUNTIME, PMG_ERR_DIVERGENCE, PMG_ERR_CUDA = range(5)
 PMG_F64, PMG_F32 = 0, 1

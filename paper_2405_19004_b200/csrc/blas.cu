@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(RED_THREADS)
 template <typename T>
 __global__ void fill_kernel(T *x, int64_t n, T v)
 {
+  pdl_prologue();
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     x[i] = v;
@@ -130,7 +131,7 @@ void launch_fill(T *x, int64_t n, T v, int sm_count, cudaStream_t s)
 {
   if (n == 0)
     return;
-  fill_kernel<T><<<ew_grid(n, sm_count), 256, 0, s>>>(x, n, v);
+  pdl_launch(fill_kernel<T>, ew_grid(n, sm_count), 256, 0, s, x, n, v);
   check_launch("fill_kernel");
 }
 

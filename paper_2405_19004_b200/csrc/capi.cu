@@ -82,6 +82,7 @@ struct pmg_level_s
   DevBuf naive_mats;      // Mif | Aif | S (T) for the straightforward kernel
   DevBuf naive_scratch;
   DevBuf tA, tB;          // transfer scratch (used when this level is the fine one)
+  DevBuf sweep_sync;      // ticket / exit / per-(colour, plane) counters of the sweep kernel
   DevBuf red;             // reduction partials + result (double)
   DevBuf io[3];           // staging for the *_host entry points
   cudaStream_t io_stream = nullptr;
@@ -346,9 +347,45 @@ void smooth_color_slab_impl(pmg_level_s *l, int variant, int color, T *x, const 
     throw InvalidArg("slab smoother: fused or boundary variant only");
 }
 
+// one persistent launch for all colours of a step (smoother_plane.cuh
+// vp_sweep_plane_kernel), when this (dim, degree, variant) has one
+template <typename T>
+bool sweep_impl(pmg_level_s *l, int variant, T *x, const T *b, cudaStream_t s)
+{
+  const int impl = smoother_impl_choice();
+  // measured slower than per-colour launches (per-tile ticket / counter
+  // traffic outweighs the saved tails): opt-in only
+  if (impl != SMOOTHER_IMPL_SWEEP || l->S.dim != 3 ||
+      !(variant == PMG_FUSED || variant == PMG_BOUNDARY))
+    return false;
+  const auto &kt = ktab<T>(l);
+  if (!kt.sweep || kt.sweep_pb <= 0)
+    return false;
+  SweepArgs<T> sw{};
+  sw.ncolors = 1 << l->S.dim;
+  sw.nv = l->S.n + 1;
+  sw.start[0] = 0;
+  for (int c = 0; c < sw.ncolors; ++c)
+  {
+    sw.c[c] = color_args<T>(l, c, x, b);
+    sw.ntx[c] = (sw.c[c].np[0] + kt.sweep_pb - 1) / kt.sweep_pb;
+    sw.start[c + 1] = sw.start[c] + sw.ntx[c] * sw.c[c].np[1] * sw.c[c].np[2];
+  }
+  const size_t need = static_cast<size_t>(2 + sw.ncolors * sw.nv) * sizeof(int);
+  if (l->sweep_sync.bytes < need)
+  {
+    l->sweep_sync.ensure(need);
+    check_cuda(cudaMemsetAsync(l->sweep_sync.p, 0, need, s), "sweep counters");
+  }
+  sw.sync = l->sweep_sync.as<int>();
+  return kt.sweep(l->patch_mats.data(), sw, variant == PMG_FUSED ? MODE_FUSED : MODE_BOUNDARY, l->sm_count, s);
+}
+
 template <typename T>
 void smooth_impl(pmg_level_s *l, int variant, T *x, const T *b, cudaStream_t s)
 {
+  if (sweep_impl<T>(l, variant, x, b, s))
+    return;
   for (int color = 0; color < (1 << l->S.dim); ++color)
     smooth_color_impl<T>(l, variant, color, x, b, s);
 }
@@ -644,9 +681,9 @@ int64_t pmg_launch_count(void) { return g_launches.load(); }
 
 int pmg_set_smoother_impl(int impl)
 {
-  if (impl < SMOOTHER_IMPL_AUTO || impl > SMOOTHER_IMPL_PLANE)
+  if (impl < SMOOTHER_IMPL_AUTO || impl > SMOOTHER_IMPL_SWEEP)
   {
-    g_last_error = "pmg_set_smoother_impl: impl must be 0, 1 or 2";
+    g_last_error = "pmg_set_smoother_impl: impl must be 0, 1, 2 or 3";
     return PMG_ERR_INVALID;
   }
   g_smoother_impl.store(impl);

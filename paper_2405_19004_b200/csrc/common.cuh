@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace pmgb
 {
@@ -33,10 +34,42 @@ enum : int
 {
   SMOOTHER_IMPL_AUTO = 0,
   SMOOTHER_IMPL_LINE = 1,
-  SMOOTHER_IMPL_PLANE = 2
+  SMOOTHER_IMPL_PLANE = 2,  // plane kernel, one launch per colour
+  SMOOTHER_IMPL_SWEEP = 3   // plane kernel, all colours in one persistent launch
 };
 int smoother_impl_choice();
 void check_launch(const char *what);  // cudaGetLastError + count
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (sm_90+): kernels launched with pdl_launch may
+// be scheduled while their predecessor in the stream is still draining; each
+// such kernel calls pdl_prologue() before touching global memory, which waits
+// for the predecessor grid to complete (and its writes to be visible), then
+// lets its own successor start launching. Hides the launch gap between the
+// 2^d colour sweeps and the short V-cycle kernels.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_prologue()
+{
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args &&...args)
+{
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  check_cuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
 
 // true the first time it is called for the current device with this mask
 // (per-function attribute setup such as the dynamic shared-memory limit)
@@ -129,6 +162,17 @@ struct ColorArgs
   int np[3];      // patches of this colour per direction
   int vb[3];      // vertex coordinate v_a = 2 j_a + vb[a]
   int total;      // patches in this colour
+};
+
+template <typename T>
+struct SweepArgs
+{
+  ColorArgs<T> c[8];  // per-colour geometry (np, vb); x, b, inv, m shared
+  int ntx[8];         // tiles per x-row of colour c
+  int start[9];       // first ticket of colour c
+  int ncolors;
+  int nv;             // vertex planes (counter stride)
+  int *sync;          // [0] ticket, [1] exit count, [2 + c nv + v2] finished tiles
 };
 
 }  // namespace pmgb

@@ -12,6 +12,10 @@ struct KernelTable
 {
   // P: PatchMatsEO<T,K>*; mode: MODE_*
   void (*smooth)(const void *P, const ColorArgs<T> &a, int mode, int sm_count, cudaStream_t s) = nullptr;
+  // whole smoothing step in one persistent launch (3D fused / boundary, where
+  // available): returns false when this (dim, degree) has no sweep kernel
+  bool (*sweep)(const void *P, const SweepArgs<T> &sw, int mode, int sm_count, cudaStream_t s) = nullptr;
+  int sweep_pb = 0;  // patches per tile of the sweep kernel
   // B: BandMats<T,K>*; b == nullptr -> y = A x, else y = b - A x
   void (*level_op)(const void *B, const T *x, const T *b, T *y, int64_t m, int sm_count,
                    cudaStream_t s) = nullptr;

@@ -32,7 +32,7 @@ void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, 
   {
     // degree 1: point-stencil kernel (smoother_point.cuh); the stencil follows
     // the even-odd matrices in the level's parameter blob (capi.cu level_init)
-    if (impl == SMOOTHER_IMPL_AUTO && (mode == MODE_FUSED || mode == MODE_BOUNDARY))
+    if ((impl == SMOOTHER_IMPL_AUTO || impl == SMOOTHER_IMPL_SWEEP) && (mode == MODE_FUSED || mode == MODE_BOUNDARY))
     {
       const auto &st = *reinterpret_cast<const PointStencil<T> *>(static_cast<const unsigned char *>(P) +
                                                                    sizeof(PatchMatsEO<T, 1>));
@@ -55,6 +55,23 @@ void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, 
     }
   }
   launch_vp_smooth_mode<D, PMG_K, T>(PM, a, mode, sm_count, s);
+}
+
+template <int D, typename T>
+bool sweep_entry(const void *P, const SweepArgs<T> &sw, int mode, int sm_count, cudaStream_t s)
+{
+  if constexpr (D == 3 && PMG_K == 2)
+  {
+    const auto &PM = *static_cast<const PatchMatsEO<T, PMG_K> *>(P);
+    if (mode == MODE_FUSED)
+      launch_vp_sweep_plane<PMG_K, T, MODE_FUSED>(PM, sw, sm_count, s);
+    else if (mode == MODE_BOUNDARY)
+      launch_vp_sweep_plane<PMG_K, T, MODE_BOUNDARY>(PM, sw, sm_count, s);
+    else
+      return false;
+    return true;
+  }
+  return false;
 }
 
 template <int D, typename T>
@@ -84,6 +101,8 @@ KernelTable<T> make_table()
 {
   KernelTable<T> t;
   t.smooth = &smooth_entry<D, T>;
+  t.sweep = &sweep_entry<D, T>;
+  t.sweep_pb = PMG_K == 2 ? PlaneCfg<2, T>::PB : 0;
   t.level_op = &op_entry<D, T>;
   t.prolongate = &prol_entry<D, T>;
   t.restrict_ = &rest_entry<D, T>;

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(32 * op_t1<K, T>())
     level_op3d_kernel(const __grid_constant__ BandMats<T, K> B, const T *__restrict__ x,
                       const T *__restrict__ b, T *__restrict__ y, int64_t m, int zchunk)
 {
+  pdl_prologue();
   constexpr int T0 = 32, T1 = op_t1<K, T>(), NT = T0 * T1, W = 2 * K + 1, R = 2 * K + 1;
   constexpr int XW = T0 + 2 * K, XH = T1 + 2 * K;
   constexpr int ROWS = (XH + T1 - 1) / T1;  // dir-0 rows per thread
@@ -218,6 +219,7 @@ __global__ void __launch_bounds__(128)
     level_op2d_kernel(const __grid_constant__ BandMats<T, K> B, const T *__restrict__ x,
                       const T *__restrict__ b, T *__restrict__ y, int64_t m, int rchunk)
 {
+  pdl_prologue();
   constexpr int T0 = 128, W = 2 * K + 1, R = 2 * K + 1, XW = T0 + 2 * K;
   __shared__ __align__(16) T Xs[2][XW];
   __shared__ T bm[K][W], ba[K][W];
@@ -343,7 +345,7 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
       check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
                  "cudaFuncSetAttribute(level_op3d carveout)");
     }
-    kern<<<dim3(gx, gy, gz), 32 * T1, smem, s>>>(B, x, b, y, m, static_cast<int>(zchunk));
+    pdl_launch(kern, dim3(gx, gy, gz), 32 * T1, smem, s, B, x, b, y, m, static_cast<int>(zchunk));
     check_launch("level_op3d_kernel");
   }
   else
@@ -355,7 +357,7 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
     rchunk = std::max<int64_t>(rchunk, std::min<int64_t>(m, 4 * K));
     const unsigned gy = static_cast<unsigned>((m + rchunk - 1) / rchunk);
     auto kern = b ? level_op2d_kernel<K, T, true> : level_op2d_kernel<K, T, false>;
-    kern<<<dim3(gx, gy), 128, 0, s>>>(B, x, b, y, m, static_cast<int>(rchunk));
+    pdl_launch(kern, dim3(gx, gy), 128, 0, s, B, x, b, y, m, static_cast<int>(rchunk));
     check_launch("level_op2d_kernel");
   }
 }

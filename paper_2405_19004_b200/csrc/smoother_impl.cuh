@@ -311,6 +311,7 @@ template <int D, int K, typename T, int MODE>
 __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
     vp_smooth_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ ColorArgs<T> a)
 {
+  pdl_prologue();
   constexpr int NC = 2 * K + 1, NI = 2 * K - 1;
   constexpr int PB = sm_pb<D, K, T>();
   constexpr int NT = sm_nt<D, K, T>();
@@ -846,7 +847,7 @@ void launch_vp_smooth(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a, int sm_
     return;
   const int grid = nbatch;  // one batch per CTA
   (void)sm_count;
-  vp_smooth_kernel<D, K, T, MODE><<<grid, NT, smem, s>>>(P, a);
+  pdl_launch(vp_smooth_kernel<D, K, T, MODE>, grid, NT, smem, s, P, a);
   check_launch("vp_smooth_kernel");
 }
 

@@ -37,7 +37,10 @@ struct PlaneCfg
   static constexpr int NC = 2 * K + 1, NI = 2 * K - 1;
   static constexpr bool F64 = sizeof(T) == 8;
   // patches per CTA: PB consecutive patches of one x-row of the colour
-  static constexpr int PB = K == 1 ? 64 : 16;
+#ifndef PMG_PLANE_PB2
+#define PMG_PLANE_PB2 16
+#endif
+  static constexpr int PB = K == 1 ? 64 : PMG_PLANE_PB2;
   // threads: the widest phase (P1: NC per patch, P2/P4: NI^2 per patch)
   static constexpr int LANES = (NC > NI * NI ? NC : NI * NI);
   static constexpr int NT = ((PB * LANES + 31) / 32) * 32;
@@ -59,31 +62,35 @@ struct PlaneCfg
   static constexpr size_t SMEM = static_cast<size_t>(PB) * (UW + WW) * sizeof(T);
 };
 
-// grid = (ceil(np0 / PB), np1, np2): CTA (bx, j1, j2) owns patches
-// j0 = bx PB + p of the colour, so the closures of its patches form one
-// contiguous box of x rows and the global -> shared copy runs along x.
+#ifndef PMG_PLANE_MINB
+#define PMG_PLANE_MINB 5
+#endif
+
+// One tile = PB consecutive patches j0 = bx PB + p (p < PB) of an x-row
+// (j1, j2) of a colour: the closures of its patches form one contiguous box of
+// x rows, so the global -> shared copy runs along x. The caller synchronises
+// before (shared memory reuse) and after (the tile's x^I stores are complete).
 template <int K, typename T, int MODE>
-__global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
-    vp_smooth_plane_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ ColorArgs<T> a)
+__device__ __forceinline__ void plane_tile(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a, int bx, int j1,
+                                           int j2, unsigned char *smem_raw)
 {
   using C = PlaneCfg<K, T>;
   constexpr int NC = C::NC, NI = C::NI, PB = C::PB, NT = C::NT, RX = C::RX;
   constexpr int UW = C::UW, SU1 = C::SU1, SU2 = C::SU2, WW = C::WW, SJ = C::SJ, SW = C::SW;
   constexpr int NI2 = NI * NI;
   constexpr int HO = K > 1 ? K - 1 : 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   T *U = reinterpret_cast<T *>(smem_raw);  // [PB][UW]  closures
   T *W = U + PB * UW;                      // [PB][WW]  work
 
   const int tid = threadIdx.x;
   const int64_t m = a.m;
   const int64_t m2 = m * m;
-  const int npv = min(PB, a.np[0] - static_cast<int>(blockIdx.x) * PB);  // valid patches
+  const int npv = min(PB, a.np[0] - bx * PB);  // valid patches
   // closure-local t = 0 per direction: g_a = k (v_a - 1) - 1, v_a = 2 j_a + vb_a
-  // (patches.cpp:71); patch p of the CTA starts at G0 + 2K p along x
-  const int G0 = K * (2 * static_cast<int>(blockIdx.x) * PB + a.vb[0] - 1) - 1;
-  const int G1 = K * (2 * static_cast<int>(blockIdx.y) + a.vb[1] - 1) - 1;
-  const int64_t G2g = static_cast<int64_t>(K) * (2 * static_cast<int64_t>(blockIdx.z) + a.vb[2] - 1) - 1;
+  // (patches.cpp:71); patch p of the tile starts at G0 + 2K p along x
+  const int G0 = K * (2 * bx * PB + a.vb[0] - 1) - 1;
+  const int G1 = K * (2 * j1 + a.vb[1] - 1) - 1;
+  const int64_t G2g = static_cast<int64_t>(K) * (2 * static_cast<int64_t>(j2) + a.vb[2] - 1) - 1;
   const int64_t G2 = G2g - a.zoff;  // local plane of t2 = 0 in x / b
 
   // ---- stage the closures of x, zero-filled outside the domain (gather,
@@ -342,6 +349,113 @@ __global__ void __launch_bounds__(PlaneCfg<K, T>::NT)
   }
 }
 
+// one launch per colour: grid = (ceil(np0 / PB), np1, np2)
+template <int K, typename T, int MODE>
+__global__ void __launch_bounds__(PlaneCfg<K, T>::NT, PMG_PLANE_MINB)
+    vp_smooth_plane_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ ColorArgs<T> a)
+{
+  pdl_prologue();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  plane_tile<K, T, MODE>(P, a, blockIdx.x, blockIdx.y, blockIdx.z, smem_raw);
+}
+
+// ---------------------------------------------------------------------------
+// All 2^d colours of one smoothing step in ONE persistent launch.
+//
+// Work items are the tiles of all colours in the reference's order (colour
+// major, smoother.cpp:54-59; within a colour z-plane major), handed out by an
+// atomic ticket. Tile (c, v2) may start once every tile of every earlier
+// colour c' < c on vertex planes v2-1 .. v2+1 has finished: those are exactly
+// the patches whose interiors intersect its closure (|v' - v| <= 1 per
+// direction, patches.cpp:71/114), so every read sees the reference's values
+// and no write overtakes an earlier colour's read. Per-patch arithmetic is
+// the per-colour kernel's, so results are bitwise identical to 2^d launches.
+// Deadlock-free without co-residency: an item only waits for items with
+// smaller tickets, all of which are held by running CTAs. The last CTA to
+// finish resets the counters, so the launch can be replayed from a graph.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int ld_acquire(const int *p)
+{
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int K, typename T, int MODE>
+__global__ void __launch_bounds__(PlaneCfg<K, T>::NT, PMG_PLANE_MINB)
+    vp_sweep_plane_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ SweepArgs<T> s)
+{
+  pdl_prologue();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int item_s;
+  int *ticket = s.sync, *exitc = s.sync + 1, *done = s.sync + 2;
+  const int total = s.start[s.ncolors];
+  if (threadIdx.x == 0)
+    item_s = atomicAdd(ticket, 1);
+  __syncthreads();
+  int item = item_s;
+  while (item < total)
+  {
+    int c = 0;
+    while (item >= s.start[c + 1])
+      ++c;
+    const ColorArgs<T> &a = s.c[c];
+    const int l = item - s.start[c];
+    const int bx = l % s.ntx[c];
+    const int rest = l / s.ntx[c];
+    const int j1 = rest % a.np[1];
+    const int j2 = rest / a.np[1];
+    const int v2 = 2 * j2 + a.vb[2];
+    // wait for the earlier colours' tiles on planes v2-1 .. v2+1 (warp 0)
+    if (threadIdx.x < 32 && c > 0)
+    {
+      const int q = threadIdx.x;  // q = 3 c' + dw
+      const int cp = q / 3, w = v2 - 1 + q % 3;
+      if (cp < c)
+      {
+        const ColorArgs<T> &b = s.c[cp];
+        const int first = b.vb[2], last = b.vb[2] + 2 * (b.np[2] - 1);
+        if (b.np[2] > 0 && w >= first && w <= last && ((w - first) & 1) == 0)
+        {
+          const int need = s.ntx[cp] * b.np[1];
+          const int *ctr = done + cp * s.nv + w;
+          while (ld_acquire(ctr) < need)
+            __nanosleep(40);
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    int next = 0;
+    if (threadIdx.x == 0)
+      next = atomicAdd(ticket, 1);  // claimed early: latency overlaps the tile
+    plane_tile<K, T, MODE>(P, a, bx, j1, j2, smem_raw);
+    __syncthreads();  // all x^I stores of the tile issued; shared memory free
+    if (threadIdx.x == 0)
+    {
+      __threadfence();
+      atomicAdd(done + c * s.nv + v2, 1);
+      item_s = next;
+    }
+    __syncthreads();
+    item = item_s;
+  }
+  // last CTA out resets the counters for the next launch
+  __shared__ int last_s;
+  if (threadIdx.x == 0)
+  {
+    __threadfence();
+    last_s = atomicAdd(exitc, 1) == static_cast<int>(gridDim.x) - 1;
+  }
+  __syncthreads();
+  if (last_s)
+  {
+    for (int i = threadIdx.x; i < 2 + s.ncolors * s.nv; i += blockDim.x)
+      s.sync[i] = 0;
+  }
+}
+
 template <int K, typename T, int MODE>
 void launch_vp_smooth_plane(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a, cudaStream_t s)
 {
@@ -359,8 +473,37 @@ void launch_vp_smooth_plane(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a, c
   if (a.total == 0)
     return;
   const dim3 grid((a.np[0] + C::PB - 1) / C::PB, a.np[1], a.np[2]);
-  vp_smooth_plane_kernel<K, T, MODE><<<grid, C::NT, C::SMEM, s>>>(P, a);
+  pdl_launch(vp_smooth_plane_kernel<K, T, MODE>, grid, C::NT, C::SMEM, s, P, a);
   check_launch("vp_smooth_plane_kernel");
+}
+
+template <int K, typename T, int MODE>
+void launch_vp_sweep_plane(const PatchMatsEO<T, K> &P, const SweepArgs<T> &sw, int sm_count, cudaStream_t s)
+{
+  using C = PlaneCfg<K, T>;
+  static unsigned attr_mask = 0;
+  static int occ[32] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (first_on_device(attr_mask))
+  {
+    check_cuda(cudaFuncSetAttribute(vp_sweep_plane_kernel<K, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(C::SMEM)),
+               "cudaFuncSetAttribute(plane sweep)");
+    check_cuda(cudaFuncSetAttribute(vp_sweep_plane_kernel<K, T, MODE>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+               "cudaFuncSetAttribute(plane sweep carveout)");
+    int o = 0;
+    check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, vp_sweep_plane_kernel<K, T, MODE>, C::NT, C::SMEM),
+               "occupancy(plane sweep)");
+    occ[dev & 31] = o > 0 ? o : 1;
+  }
+  const int total = sw.start[sw.ncolors];
+  if (total == 0)
+    return;
+  const int grid = std::min(total, occ[dev & 31] * sm_count);
+  pdl_launch(vp_sweep_plane_kernel<K, T, MODE>, grid, C::NT, C::SMEM, s, P, sw);
+  check_launch("vp_sweep_plane_kernel");
 }
 
 }  // namespace pmgb

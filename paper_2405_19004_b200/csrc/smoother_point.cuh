@@ -31,6 +31,7 @@ template <int D, typename T, int MODE>
 __global__ void __launch_bounds__(128) vp_point_kernel(const __grid_constant__ PointStencil<T> st,
                                                        const __grid_constant__ ColorArgs<T> a)
 {
+  pdl_prologue();
   const int j0 = blockIdx.x * 32 + threadIdx.x;
   const int j1 = blockIdx.y * 4 + threadIdx.y;
   const int j2 = D == 3 ? static_cast<int>(blockIdx.z) : 0;
@@ -87,7 +88,7 @@ void launch_vp_point(const PointStencil<T> &st, const ColorArgs<T> &a, cudaStrea
     return;
   dim3 block(32, 4, 1);
   dim3 grid((a.np[0] + 31) / 32, (a.np[1] + 3) / 4, D == 3 ? a.np[2] : 1);
-  vp_point_kernel<D, T, MODE><<<grid, block, 0, s>>>(st, a);
+  pdl_launch(vp_point_kernel<D, T, MODE>, grid, block, 0, s, st, a);
   check_launch("vp_point_kernel");
 }
 

@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(256)
     prolong_pass_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ in,
                         T *__restrict__ out, int64_t e0, int64_t e1, int64_t e2, int64_t mc)
 {
+  pdl_prologue();
   __shared__ T Ps[2 * K + 1][K + 1];
   for (int e = threadIdx.x; e < (2 * K + 1) * (K + 1); e += blockDim.x)
     (&Ps[0][0])[e] = (&P.P[0][0])[e];
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(256)
     restrict_pass_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ in,
                          T *__restrict__ out, int64_t e0, int64_t e1, int64_t e2, int64_t mf)
 {
+  pdl_prologue();
   __shared__ T Ps[2 * K + 1][K + 1];
   for (int e = threadIdx.x; e < (2 * K + 1) * (K + 1); e += blockDim.x)
     (&Ps[0][0])[e] = (&P.P[0][0])[e];
@@ -149,24 +151,24 @@ void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, in
   const int64_t mf = 2 * mc + 1;
   if constexpr (D == 2)
   {
-    prolong_pass_kernel<K, T, 0, false><<<pass_grid(mf * mc, sm_count), 256, 0, s>>>(P, xc, tA, mf, mc, 1, mc);
+    pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf * mc, sm_count), 256, 0, s, P, xc, tA, mf, mc, 1, mc);
     check_launch("prolong_pass0");
     if (acc)
-      prolong_pass_kernel<K, T, 1, true><<<pass_grid(mf * mf, sm_count), 256, 0, s>>>(P, tA, xf, mf, mf, 1, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 1, true>, pass_grid(mf * mf, sm_count), 256, 0, s, P, tA, xf, mf, mf, 1, mc);
     else
-      prolong_pass_kernel<K, T, 1, false><<<pass_grid(mf * mf, sm_count), 256, 0, s>>>(P, tA, xf, mf, mf, 1, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf * mf, sm_count), 256, 0, s, P, tA, xf, mf, mf, 1, mc);
     check_launch("prolong_pass1");
   }
   else
   {
-    prolong_pass_kernel<K, T, 0, false><<<pass_grid(mf * mc * mc, sm_count), 256, 0, s>>>(P, xc, tA, mf, mc, mc, mc);
+    pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf * mc * mc, sm_count), 256, 0, s, P, xc, tA, mf, mc, mc, mc);
     check_launch("prolong_pass0");
-    prolong_pass_kernel<K, T, 1, false><<<pass_grid(mf * mf * mc, sm_count), 256, 0, s>>>(P, tA, tB, mf, mf, mc, mc);
+    pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf * mf * mc, sm_count), 256, 0, s, P, tA, tB, mf, mf, mc, mc);
     check_launch("prolong_pass1");
     if (acc)
-      prolong_pass_kernel<K, T, 2, true><<<pass_grid(mf * mf * mf, sm_count), 256, 0, s>>>(P, tB, xf, mf, mf, mf, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 2, true>, pass_grid(mf * mf * mf, sm_count), 256, 0, s, P, tB, xf, mf, mf, mf, mc);
     else
-      prolong_pass_kernel<K, T, 2, false><<<pass_grid(mf * mf * mf, sm_count), 256, 0, s>>>(P, tB, xf, mf, mf, mf, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 2, false>, pass_grid(mf * mf * mf, sm_count), 256, 0, s, P, tB, xf, mf, mf, mf, mc);
     check_launch("prolong_pass2");
   }
 }
@@ -178,18 +180,18 @@ void launch_restrict(const ProlMats<T, K> &P, const T *rf, T *rc, int64_t mc, T 
   const int64_t mf = 2 * mc + 1;
   if constexpr (D == 2)
   {
-    restrict_pass_kernel<K, T, 0><<<pass_grid(mc * mf, sm_count), 256, 0, s>>>(P, rf, tA, mc, mf, 1, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc * mf, sm_count), 256, 0, s, P, rf, tA, mc, mf, 1, mf);
     check_launch("restrict_pass0");
-    restrict_pass_kernel<K, T, 1><<<pass_grid(mc * mc, sm_count), 256, 0, s>>>(P, tA, rc, mc, mc, 1, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc * mc, sm_count), 256, 0, s, P, tA, rc, mc, mc, 1, mf);
     check_launch("restrict_pass1");
   }
   else
   {
-    restrict_pass_kernel<K, T, 0><<<pass_grid(mc * mf * mf, sm_count), 256, 0, s>>>(P, rf, tA, mc, mf, mf, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc * mf * mf, sm_count), 256, 0, s, P, rf, tA, mc, mf, mf, mf);
     check_launch("restrict_pass0");
-    restrict_pass_kernel<K, T, 1><<<pass_grid(mc * mc * mf, sm_count), 256, 0, s>>>(P, tA, tB, mc, mc, mf, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc * mc * mf, sm_count), 256, 0, s, P, tA, tB, mc, mc, mf, mf);
     check_launch("restrict_pass1");
-    restrict_pass_kernel<K, T, 2><<<pass_grid(mc * mc * mc, sm_count), 256, 0, s>>>(P, tB, rc, mc, mc, mc, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 2>, pass_grid(mc * mc * mc, sm_count), 256, 0, s, P, tB, rc, mc, mc, mc, mf);
     check_launch("restrict_pass2");
   }
 }

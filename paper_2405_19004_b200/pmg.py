@@ -39,14 +39,15 @@ __all__ = [
     "DivergenceError", "set_smoother_impl", "get_smoother_impl",
 ]
 
-_SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2}
+_SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2, "sweep": 3}
 
 
 def set_smoother_impl(impl: str = "auto") -> None:
     """Select the smoother kernel organisation for later calls (A/B
     measurement; no reference counterpart): "auto" (per-degree default),
-    "line" (line-per-thread kernel) or "plane" (plane-streaming kernel, 3D
-    fused/boundary, degree <= 3)."""
+    "line" (line-per-thread kernel everywhere), "plane" (plane-streaming
+    kernel, 3D fused/boundary, degree <= 2, one launch per colour) or "sweep"
+    (the plane kernel with all colours of a step in one persistent launch)."""
     if impl not in _SMOOTHER_IMPLS:
         raise ValueError(f"smoother impl must be one of {sorted(_SMOOTHER_IMPLS)}")
     check(_lib.load().pmg_set_smoother_impl(_SMOOTHER_IMPLS[impl]), "set_smoother_impl")

@@ -256,7 +256,7 @@ def test_cpp_shim(pmg, cuda):
 # plane-streaming) against the reference, including levels whose colour sizes
 # are not multiples of the patches-per-CTA (ragged last CTA) and level 1
 # (a single patch, the coarse solve).
-@pytest.mark.parametrize("impl", ["auto", "line", "plane"])
+@pytest.mark.parametrize("impl", ["auto", "line", "plane", "sweep"])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 @pytest.mark.parametrize("case", [(2, 1, 1), (2, 1, 6), (3, 1, 1), (3, 1, 5), (3, 2, 1), (3, 2, 3), (3, 2, 5), (3, 3, 1), (3, 3, 4)],
                          ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")
@@ -275,3 +275,33 @@ def test_smoother_impls(pmg, cuda, case, dtype, impl):
             assert rel(xd.cpu().numpy(), want) < TOL[dtype], (variant, rel(xd.cpu().numpy(), want))
     finally:
         pmg.set_smoother_impl("auto")
+
+
+# The persistent all-colour sweep must reproduce the per-colour launches
+# bitwise (same per-patch arithmetic, same colour order), over several steps
+# (the counters are reset by the last CTA of each launch) and inside a
+# graph-captured V-cycle.
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("L", [2, 3, 4, 5])
+def test_sweep_bitwise(pmg, cuda, L, dtype):
+    dim, k = 3, 2
+    ctx = pmg.make_multigrid_context(dim, k, L, dtype=dtype)
+    lev = ctx.levels[-1]
+    x0, b = inputs(lev.level.total_dofs, dtype, seed=11)
+    out = {}
+    try:
+        for impl in ["plane", "sweep"]:
+            pmg.set_smoother_impl(impl)
+            xd = dev(cuda, x0.copy())
+            bd = dev(cuda, b)
+            for _ in range(3):
+                for variant in ["fused", "boundary"]:
+                    pmg.smooth(lev, xd, bd, variant)
+            xv = dev(cuda, x0.copy())
+            for _ in range(2):
+                pmg.v_cycle(ctx, L - 1, xv, bd, use_graph=True)
+            out[impl] = (xd.cpu().numpy(), xv.cpu().numpy())
+    finally:
+        pmg.set_smoother_impl("auto")
+    assert np.array_equal(out["plane"][0], out["sweep"][0])
+    assert np.array_equal(out["plane"][1], out["sweep"][1])
