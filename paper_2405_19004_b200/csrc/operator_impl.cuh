@@ -25,18 +25,35 @@
 namespace pmgb
 {
 
+// ---------------------------------------------------------------------------
+// 3D: CTA = 32 x 8 output columns, marching over a z chunk (a multiple of k,
+// so the lattice residue of every plane, and with it the dir-2 band row, is a
+// compile-time constant of the k-fold unrolled plane loop).
+//   per input plane q (3-deep cp.async ring; each thread copies fixed tile
+//   slots whose in-plane offsets are computed once):
+//     dir 0: zM = M0 x, zA = A0 x on the (8+2k) x 32 rows (band row of the
+//            lane's x residue in registers)
+//     dir 1: wM = M1 zM, wS = A1 zM + M1 zA (band row of the warp's y residue)
+//     dir 2: acc[j] += A2[p][q] wM + M2[p][q] wS for the 2k+1 output planes
+//            p = q-k+j (register shift ring); plane q-k is complete: y = b - acc[0].
+// One barrier per plane. Deterministic, no atomics.
+// ---------------------------------------------------------------------------
 template <int K, typename T>
-constexpr int op_t1()
+struct Op3Cfg
 {
-  return 8;
-}
+  static constexpr int TX = 32, TY = 8, NT = TX * TY, W = 2 * K + 1;
+  static constexpr int XW = TX + 2 * K, XH = TY + 2 * K, XN = XW * XH;
+  static constexpr int NLOAD = (XN + NT - 1) / NT;   // tile slots per thread
+  static constexpr int ROWS = (XH + TY - 1) / TY;    // dir-0 rows per thread
+  static constexpr bool C1REG = K <= 2;              // dir-1 band row in registers
+  static constexpr size_t SMEM =
+      sizeof(T) * (3 * static_cast<size_t>(XN) + 3 * NT + 4 * static_cast<size_t>(XH) * TX + 2 * K * W);
+};
 
 template <int K, typename T>
 constexpr size_t op3d_smem()
 {
-  constexpr int T0 = 32, T1 = op_t1<K, T>(), W = 2 * K + 1;
-  constexpr int XW = T0 + 2 * K, XH = T1 + 2 * K;
-  return sizeof(T) * (3 * static_cast<size_t>(XH) * XW + 3 * T1 * T0 + 4 * XH * T0 + 2 * K * W);
+  return Op3Cfg<K, T>::SMEM;
 }
 
 template <typename T>
@@ -51,165 +68,207 @@ __device__ __forceinline__ void op_cp_async(T *smem, const T *gmem, bool valid)
                  : "memory");
 }
 
+// two resident CTAs per SM for k >= 3 (measured: register-capped 128 beats
+// the unconstrained 130-214 registers; for k <= 2 the compiler's choice wins)
+template <int K>
+constexpr int op3d_minb()
+{
+  return K >= 3 ? 2 : 1;
+}
+
 template <int K, typename T, bool RESID>
-__global__ void __launch_bounds__(32 * op_t1<K, T>())
+__global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
     level_op3d_kernel(const __grid_constant__ BandMats<T, K> B, const T *__restrict__ x,
                       const T *__restrict__ b, T *__restrict__ y, int64_t m, int zchunk)
 {
   pdl_prologue();
-  constexpr int T0 = 32, T1 = op_t1<K, T>(), NT = T0 * T1, W = 2 * K + 1, R = 2 * K + 1;
-  constexpr int XW = T0 + 2 * K, XH = T1 + 2 * K;
-  constexpr int ROWS = (XH + T1 - 1) / T1;  // dir-0 rows per thread
+  using C = Op3Cfg<K, T>;
+  constexpr int TX = C::TX, TY = C::TY, NT = C::NT, W = C::W, XW = C::XW, XH = C::XH, XN = C::XN;
+  constexpr int NLOAD = C::NLOAD, ROWS = C::ROWS;
   extern __shared__ __align__(16) unsigned char smraw[];
-  T *Xs = reinterpret_cast<T *>(smraw);  // [3][XH][XW]  input planes (3-deep pipeline)
-  T *Bv = Xs + 3 * XH * XW;              // [3][T1][T0]  b of the output planes
-  T *ZM = Bv + 3 * T1 * T0;              // [2][XH][T0]
-  T *ZA = ZM + 2 * XH * T0;              // [2][XH][T0]
-  T *bm = ZA + 2 * XH * T0;              // [K][W]
+  T *Xs = reinterpret_cast<T *>(smraw);  // [3][XH][XW]  input planes
+  T *Bv = Xs + 3 * XN;                   // [3][NT]      b of the output planes
+  T *ZM = Bv + 3 * NT;                   // [2][XH][TX]
+  T *ZA = ZM + 2 * XH * TX;              // [2][XH][TX]
+  T *bm = ZA + 2 * XH * TX;              // [K][W]
   T *ba = bm + K * W;
 
   const int tid = threadIdx.x;
+  const int lane = tid % TX, wy = tid / TX;
   for (int e = tid; e < K * W; e += NT)
   {
     bm[e] = (&B.M[0][0])[e];
     ba[e] = (&B.A[0][0])[e];
   }
-  const int64_t g0 = static_cast<int64_t>(blockIdx.x) * T0;
-  const int64_t g1 = static_cast<int64_t>(blockIdx.y) * T1;
-  const int64_t zs = static_cast<int64_t>(blockIdx.z) * zchunk;
+  const int g0 = static_cast<int>(blockIdx.x) * TX;
+  const int g1 = static_cast<int>(blockIdx.y) * TY;
+  const int64_t zs = static_cast<int64_t>(blockIdx.z) * zchunk;  // multiple of K
   const int64_t ze = min(zs + zchunk, m);
-  const int i = tid % T0, jj = tid / T0;
-  __syncthreads();
-  T c0m[W], c0a[W], c1m[W], c1a[W];
+  const int64_t m2 = m * m;
+  // this thread's tile slots: in-plane offset and validity (fixed for all planes)
+  int off[NLOAD];
+  unsigned okm = 0;
+#pragma unroll
+  for (int j = 0; j < NLOAD; ++j)
   {
-    const int res0 = static_cast<int>((g0 + i + 1) % K);
-    const int res1 = static_cast<int>((g1 + jj + 1) % K);
+    const int e = tid + j * NT;
+    const int jr = e / XW, ir = e - (e / XW) * XW;
+    const int gx = g0 - K + ir, gy = g1 - K + jr;
+    const bool ok = e < XN && gx >= 0 && gx < m && gy >= 0 && gy < m;
+    off[j] = ok ? gy * static_cast<int>(m) + gx : 0;
+    okm |= (ok ? 1u : 0u) << j;
+  }
+  const bool out_ok = (g0 + lane < m) && (g1 + wy < m);
+  const int out_off = (g1 + wy) * static_cast<int>(m) + g0 + lane;
+  __syncthreads();
+  T c0m[W], c0a[W];
+  {
+    const int res0 = (g0 + lane + 1) % K;
 #pragma unroll
     for (int o = 0; o < W; ++o)
     {
       c0m[o] = bm[res0 * W + o];
       c0a[o] = ba[res0 * W + o];
-      c1m[o] = bm[res1 * W + o];
-      c1a[o] = ba[res1 * W + o];
     }
   }
-  const bool out_ok = (g0 + i < m) && (g1 + jj < m);
+  const int res1 = (g1 + wy + 1) % K;
+  T c1r_m[C::C1REG ? W : 1], c1r_a[C::C1REG ? W : 1];
+  if constexpr (C::C1REG)
+  {
+#pragma unroll
+    for (int o = 0; o < W; ++o)
+    {
+      c1r_m[o] = bm[res1 * W + o];
+      c1r_a[o] = ba[res1 * W + o];
+    }
+  }
+  const T *c1s_m = bm + res1 * W, *c1s_a = ba + res1 * W;
   const int NPL = static_cast<int>(ze - zs) + 2 * K;  // input planes zs-K .. ze+K-1
 
-  // pipeline group `it`: input plane q = zs-K+it (x tile, zero outside) and,
-  // for the residual, b of the output plane emitted at iteration it (q - K)
   auto issue = [&](int it) {
     const int64_t q = zs - K + it;
     const bool zin = q >= 0 && q < m;
-    T *dst = Xs + (it % 3) * XH * XW;
-    for (int e = tid; e < XH * XW; e += NT)
+    T *dst = Xs + (it % 3) * XN;
+    const T *xq = x + (zin ? q : 0) * m2;
+#pragma unroll
+    for (int j = 0; j < NLOAD; ++j)
     {
-      const int jr = e / XW, ir = e - jr * XW;
-      const int64_t gx = g0 - K + ir, gy = g1 - K + jr;
-      const bool ok = zin && gx >= 0 && gx < m && gy >= 0 && gy < m;
-      op_cp_async(dst + e, ok ? x + (q * m + gy) * m + gx : x, ok);
+      const int e = tid + j * NT;
+      if (e < XN)
+      {
+        const bool ok = zin && ((okm >> j) & 1u);
+        op_cp_async(dst + e, xq + off[j], ok);
+      }
     }
     if constexpr (RESID)
     {
       const int64_t p = q - K;
       const bool ok = out_ok && it >= 2 * K && p < ze;
-      op_cp_async(Bv + (it % 3) * NT + tid, ok ? b + (p * m + g1 + jj) * m + g0 + i : b, ok);
+      op_cp_async(Bv + (it % 3) * NT + tid, ok ? b + p * m2 + out_off : b, ok);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
-  T acc[R];
+  T acc[W];
 #pragma unroll
-  for (int o = 0; o < R; ++o)
+  for (int o = 0; o < W; ++o)
     acc[o] = T(0);
 
   issue(0);
   if (NPL > 1)
+  {
     issue(1);
-  if (NPL > 1)
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  }
   else
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
 
-  for (int base = 0; base < NPL; base += R)
+  for (int base = 0; base < NPL; base += K)
   {
 #pragma unroll
-    for (int u = 0; u < R; ++u)
+    for (int u = 0; u < K; ++u)
     {
       const int it = base + u;  // uniform across the CTA
-      if (it < NPL)
+      if (it >= NPL)
+        break;
+      if (it + 2 < NPL)
+        issue(it + 2);
+      // dir 0
+      const T *xs = Xs + (it % 3) * XN;
+      T *zm = ZM + (it & 1) * XH * TX;
+      T *za = ZA + (it & 1) * XH * TX;
+#pragma unroll
+      for (int rr = 0; rr < ROWS; ++rr)
       {
-        const int bi = it % 3;
-        const int zb = it & 1;
-        const int64_t q = zs - K + it;
-        if (it + 2 < NPL)
-          issue(it + 2);
-        const int64_t p_out = q - K;
-        const bool emit = it >= 2 * K && p_out < ze;
-        // dir 0: rows jj, jj+T1, ... of the tile
-        const T *xs = Xs + bi * XH * XW;
-        T *zm = ZM + zb * XH * T0;
-        T *za = ZA + zb * XH * T0;
-#pragma unroll
-        for (int rr = 0; rr < ROWS; ++rr)
+        const int j = wy + rr * TY;
+        if (j < XH)
         {
-          const int j = jj + rr * T1;
-          if (j < XH)
+          // two interleaved partial sums per output: halves the FMA chain
+          const T *xr = xs + j * XW + lane;
+          T vm0 = c0m[0] * xr[0], va0 = c0a[0] * xr[0];
+          T vm1 = c0m[1] * xr[1], va1 = c0a[1] * xr[1];
+#pragma unroll
+          for (int o = 2; o < W; o += 2)
           {
-            const T *xr = xs + j * XW + i;
-            T vm = c0m[0] * xr[0], va = c0a[0] * xr[0];
-#pragma unroll
-            for (int o = 1; o < W; ++o)
+            vm0 = fma(c0m[o], xr[o], vm0);
+            va0 = fma(c0a[o], xr[o], va0);
+            if (o + 1 < W)
             {
-              vm = fma(c0m[o], xr[o], vm);
-              va = fma(c0a[o], xr[o], va);
+              vm1 = fma(c0m[o + 1], xr[o + 1], vm1);
+              va1 = fma(c0a[o + 1], xr[o + 1], va1);
             }
-            zm[j * T0 + i] = vm;
-            za[j * T0 + i] = va;
           }
+          zm[j * TX + lane] = vm0 + vm1;
+          za[j * TX + lane] = va0 + va1;
         }
-        // group it+1 complete (it+2 may stay in flight); all dir-0 rows visible
-        if (it + 2 < NPL)
-          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        else
-          asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        __syncthreads();
-        // dir 1
-        T wm = T(0), ws = T(0);
-#pragma unroll
-        for (int o = 0; o < W; ++o)
-        {
-          const T vm = zm[(jj + o) * T0 + i], va = za[(jj + o) * T0 + i];
-          wm = fma(c1m[o], vm, wm);
-          ws = fma(c1a[o], vm, ws);
-          ws = fma(c1m[o], va, ws);
-        }
-        // dir 2: input plane q feeds output planes p = q - K + oo (oo = 0..2K)
-        // with coefficient band[res(p)][q - p + K] = band[res(p)][2K - oo];
-        // the ring slot of output plane index (it - K + oo) is static
-        const int rq = static_cast<int>(((q + 1) % K + K) % K);  // residue of plane q
-#pragma unroll
-        for (int oo = 0; oo < W; ++oo)
-        {
-          int res = rq + (oo % K);  // residue of output plane q - K + oo
-          if (res >= K)
-            res -= K;
-          const int slot = ((u - K + oo) % R + R) % R;
-          acc[slot] = fma(ba[res * W + (2 * K - oo)], wm, acc[slot]);
-          acc[slot] = fma(bm[res * W + (2 * K - oo)], ws, acc[slot]);
-        }
-        const int sl_out = ((u - K) % R + R) % R;
-        if (emit && out_ok)
-        {
-          const int64_t idx = (p_out * m + g1 + jj) * m + g0 + i;
-          if constexpr (RESID)
-            y[idx] = Bv[bi * NT + tid] - acc[sl_out];
-          else
-            y[idx] = acc[sl_out];
-        }
-        acc[sl_out] = T(0);
       }
+      if (it + 2 < NPL)
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
+      // dir 1
+      T wm = T(0), ws = T(0), ws2 = T(0), wm2 = T(0);
+#pragma unroll
+      for (int o = 0; o < W; ++o)
+      {
+        const T vm = zm[(wy + o) * TX + lane], va = za[(wy + o) * TX + lane];
+        const T cm = C::C1REG ? c1r_m[C::C1REG ? o : 0] : c1s_m[o];
+        const T ca = C::C1REG ? c1r_a[C::C1REG ? o : 0] : c1s_a[o];
+        if (o & 1)
+          wm2 = fma(cm, vm, wm2);
+        else
+          wm = fma(cm, vm, wm);
+        ws = fma(ca, vm, ws);
+        ws2 = fma(cm, va, ws2);
+      }
+      wm += wm2;
+      ws += ws2;
+      // dir 2: output plane p = q - K + jo, lattice residue (p + 1) mod K =
+      // (u + 1 + jo) mod K; band offset q - p + K = 2K - jo
+#pragma unroll
+      for (int jo = 0; jo < W; ++jo)
+      {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int res = (u + 1 + jo) % K;
+        acc[jo] = fma(B.A[res][2 * K - jo], wm, acc[jo]);
+        acc[jo] = fma(B.M[res][2 * K - jo], ws, acc[jo]);
+      }
+      const int64_t p_out = zs - 2 * K + it;
+      if (it >= 2 * K && p_out < ze && out_ok)
+      {
+        const int64_t idx = p_out * m2 + out_off;
+        if constexpr (RESID)
+          y[idx] = Bv[(it % 3) * NT + tid] - acc[0];
+        else
+          y[idx] = acc[0];
+      }
+#pragma unroll
+      for (int jo = 0; jo < W - 1; ++jo)
+        acc[jo] = acc[jo + 1];
+      acc[W - 1] = T(0);
     }
   }
 }
@@ -325,15 +384,17 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
 {
   if constexpr (D == 3)
   {
-    constexpr int T1 = op_t1<K, T>();
-    constexpr size_t smem = op3d_smem<K, T>();
-    const unsigned gx = static_cast<unsigned>((m + 31) / 32);
-    const unsigned gy = static_cast<unsigned>((m + T1 - 1) / T1);
-    // z chunk: enough CTAs for ~6 per SM, but >= 4k planes to bound the halo
+    using C = Op3Cfg<K, T>;
+    constexpr size_t smem = C::SMEM;
+    const unsigned gx = static_cast<unsigned>((m + C::TX - 1) / C::TX);
+    const unsigned gy = static_cast<unsigned>((m + C::TY - 1) / C::TY);
+    // z chunk (a multiple of K): enough CTAs for ~6 per SM, >= 4k planes to
+    // bound the recomputed halo
     int64_t want = static_cast<int64_t>(sm_count) * 6;
     int64_t nz = (want + gx * gy - 1) / (gx * gy);
     int64_t zchunk = (m + nz - 1) / nz;
-    zchunk = std::max<int64_t>(zchunk, std::min<int64_t>(m, 4 * K));
+    zchunk = std::max<int64_t>(zchunk, 4 * K);
+    zchunk = (zchunk + K - 1) / K * K;
     const unsigned gz = static_cast<unsigned>((m + zchunk - 1) / zchunk);
     auto kern = b ? level_op3d_kernel<K, T, true> : level_op3d_kernel<K, T, false>;
     static unsigned attr_mask[2] = {0, 0};
@@ -345,7 +406,7 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
       check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
                  "cudaFuncSetAttribute(level_op3d carveout)");
     }
-    pdl_launch(kern, dim3(gx, gy, gz), 32 * T1, smem, s, B, x, b, y, m, static_cast<int>(zchunk));
+    pdl_launch(kern, dim3(gx, gy, gz), C::NT, smem, s, B, x, b, y, m, static_cast<int>(zchunk));
     check_launch("level_op3d_kernel");
   }
   else
