@@ -19,8 +19,33 @@
 namespace pmgb
 {
 
-// out has extents ext_out (dir 0 fastest); along DIR the input has mc coarse
-// nodes and the output mf = 2 mc + 1 fine nodes.
+// Both pass kernels: block (32, 8), grid (ceil(e0/32), ceil(e1/8), e2), so an
+// output node's (i0, i1, i2) comes from the launch geometry (no 64-bit
+// division); along DIR the input index is strided, the other two are shared
+// with the output.
+template <int DIR>
+__device__ __forceinline__ void pass_index(int64_t e0, int64_t e1, int64_t ie0, int64_t ie1, int64_t i0,
+                                           int64_t i1, int64_t i2, int64_t &base, int64_t &stride)
+{
+  if (DIR == 0)
+  {
+    base = (i2 * ie1 + i1) * ie0;
+    stride = 1;
+  }
+  else if (DIR == 1)
+  {
+    base = i2 * ie1 * ie0 + i0;
+    stride = ie0;
+  }
+  else
+  {
+    base = i1 * ie0 + i0;
+    stride = ie0 * ie1;
+  }
+}
+
+// out has extents (e0, e1, e2) (dir 0 fastest); along DIR the input has mc
+// coarse nodes and the output mf = 2 mc + 1 fine nodes.
 template <int K, typename T, int DIR, bool ACC>
 __global__ void __launch_bounds__(256)
     prolong_pass_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ in,
@@ -28,57 +53,38 @@ __global__ void __launch_bounds__(256)
 {
   pdl_prologue();
   __shared__ T Ps[2 * K + 1][K + 1];
-  for (int e = threadIdx.x; e < (2 * K + 1) * (K + 1); e += blockDim.x)
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int e = tid; e < (2 * K + 1) * (K + 1); e += 256)
     (&Ps[0][0])[e] = (&P.P[0][0])[e];
   __syncthreads();
-  const int64_t total = e0 * e1 * e2;
-  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x)
-  {
-    int64_t i0 = idx % e0;
-    int64_t rest = idx / e0;
-    int64_t i1 = rest % e1;
-    int64_t i2 = rest / e1;
-    const int64_t ifine = DIR == 0 ? i0 : (DIR == 1 ? i1 : i2);
-    const int64_t p = ifine + 1;  // fine lattice
-    const int64_t c = (p - 1) / (2 * K);
-    const int r = static_cast<int>(p - 2 * c * K);
-    // input strides (input extent along DIR is mc)
-    const int64_t ie0 = DIR == 0 ? mc : e0;
-    const int64_t ie1 = DIR == 1 ? mc : e1;
-    int64_t base, stride;
-    if (DIR == 0)
-    {
-      base = (i2 * ie1 + i1) * ie0;
-      stride = 1;
-    }
-    else if (DIR == 1)
-    {
-      base = i2 * ie1 * ie0 + i0;
-      stride = ie0;
-    }
-    else
-    {
-      base = i1 * ie0 + i0;
-      stride = ie0 * ie1;
-    }
-    T s = T(0);
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
+  const int64_t i1 = static_cast<int64_t>(blockIdx.y) * 8 + threadIdx.y;
+  const int64_t i2 = blockIdx.z;
+  if (i0 >= e0 || i1 >= e1)
+    return;
+  const int64_t ifine = DIR == 0 ? i0 : (DIR == 1 ? i1 : i2);
+  const int p = static_cast<int>(ifine) + 1;  // fine lattice
+  const int c = (p - 1) / (2 * K);            // owner cell
+  const int r = p - 2 * c * K;
+  int64_t base, stride;
+  pass_index<DIR>(e0, e1, DIR == 0 ? mc : e0, DIR == 1 ? mc : e1, i0, i1, i2, base, stride);
+  T s = T(0);
 #pragma unroll
-    for (int t = 0; t <= K; ++t)
-    {
-      const int64_t q = c * K + t;  // coarse lattice
-      if (q >= 1 && q <= mc)
-        s = fma(Ps[r][t], in[base + (q - 1) * stride], s);
-    }
-    if constexpr (ACC)
-      out[idx] += s;
-    else
-      out[idx] = s;
+  for (int t = 0; t <= K; ++t)
+  {
+    const int q = c * K + t;  // coarse lattice
+    if (q >= 1 && q <= mc)
+      s = fma(Ps[r][t], __ldg(in + base + (q - 1) * stride), s);
   }
+  const int64_t idx = (i2 * e1 + i1) * e0 + i0;
+  if constexpr (ACC)
+    out[idx] += s;
+  else
+    out[idx] = s;
 }
 
-// out has extents ext_out; along DIR the output has mc coarse nodes and the
-// input mf fine nodes.
+// out has extents (e0, e1, e2); along DIR the output has mc coarse nodes and
+// the input mf fine nodes.
 template <int K, typename T, int DIR>
 __global__ void __launch_bounds__(256)
     restrict_pass_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ in,
@@ -86,64 +92,48 @@ __global__ void __launch_bounds__(256)
 {
   pdl_prologue();
   __shared__ T Ps[2 * K + 1][K + 1];
-  for (int e = threadIdx.x; e < (2 * K + 1) * (K + 1); e += blockDim.x)
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int e = tid; e < (2 * K + 1) * (K + 1); e += 256)
     (&Ps[0][0])[e] = (&P.P[0][0])[e];
   __syncthreads();
-  const int64_t total = e0 * e1 * e2;
-  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x)
-  {
-    int64_t i0 = idx % e0;
-    int64_t rest = idx / e0;
-    int64_t i1 = rest % e1;
-    int64_t i2 = rest / e1;
-    const int64_t icoarse = DIR == 0 ? i0 : (DIR == 1 ? i1 : i2);
-    const int64_t q = icoarse + 1;  // coarse lattice
-    const int64_t ie0 = DIR == 0 ? mf : e0;
-    const int64_t ie1 = DIR == 1 ? mf : e1;
-    int64_t base, stride;
-    if (DIR == 0)
-    {
-      base = (i2 * ie1 + i1) * ie0;
-      stride = 1;
-    }
-    else if (DIR == 1)
-    {
-      base = i2 * ie1 * ie0 + i0;
-      stride = ie0;
-    }
-    else
-    {
-      base = i1 * ie0 + i0;
-      stride = ie0 * ie1;
-    }
-    T s = T(0);
-    const int tq = static_cast<int>(q % K);
-    // cells containing coarse node q: (c, t) with q = cK + t, 0 <= t <= K
-    const int ncell = (tq == 0) ? 2 : 1;
-    for (int h = 0; h < ncell; ++h)
-    {
-      const int64_t c = (tq == 0) ? (q / K - 1 + h) : (q / K);
-      const int t = (tq == 0) ? (h == 0 ? K : 0) : tq;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
+  const int64_t i1 = static_cast<int64_t>(blockIdx.y) * 8 + threadIdx.y;
+  const int64_t i2 = blockIdx.z;
+  if (i0 >= e0 || i1 >= e1)
+    return;
+  const int64_t icoarse = DIR == 0 ? i0 : (DIR == 1 ? i1 : i2);
+  const int q = static_cast<int>(icoarse) + 1;  // coarse lattice
+  int64_t base, stride;
+  pass_index<DIR>(e0, e1, DIR == 0 ? mf : e0, DIR == 1 ? mf : e1, i0, i1, i2, base, stride);
+  T s = T(0);
+  const int tq = q % K;
+  // cells containing coarse node q: (c, t) with q = cK + t, 0 <= t <= K; the
+  // transpose of the prolongation gathers their 2K owned fine nodes
+  const int c1 = q / K;
 #pragma unroll
-      for (int r = 1; r <= 2 * K; ++r)
-      {
-        const int64_t p = 2 * c * K + r;  // fine lattice
-        if (p >= 1 && p <= mf)
-          s = fma(Ps[r][t], in[base + (p - 1) * stride], s);
-      }
+  for (int h = 0; h < 2; ++h)
+  {
+    if (h == 1 && tq != 0)
+      break;
+    const int c = (tq == 0) ? (c1 - 1 + h) : c1;
+    const int t = (tq == 0) ? (h == 0 ? K : 0) : tq;
+#pragma unroll
+    for (int r = 1; r <= 2 * K; ++r)
+    {
+      const int p = 2 * c * K + r;  // fine lattice
+      if (p >= 1 && p <= mf)
+        s = fma(Ps[r][t], __ldg(in + base + (p - 1) * stride), s);
     }
-    out[idx] = s;
   }
+  out[(i2 * e1 + i1) * e0 + i0] = s;
 }
 
-inline unsigned pass_grid(int64_t total, int sm_count)
+inline dim3 pass_grid(int64_t e0, int64_t e1, int64_t e2)
 {
-  const int64_t blocks = (total + 255) / 256;
-  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(blocks, static_cast<int64_t>(sm_count) * 32)));
+  return dim3(static_cast<unsigned>((e0 + 31) / 32), static_cast<unsigned>((e1 + 7) / 8),
+              static_cast<unsigned>(e2));
 }
 
-// xf (+)= P xc. tA, tB: scratch of at least mf*mf*mc (3D) / mf*mc (2D).
 template <int D, int K, typename T>
 void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, int64_t mc,
                        T *tA, T *tB, int sm_count, cudaStream_t s)
@@ -151,24 +141,24 @@ void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, in
   const int64_t mf = 2 * mc + 1;
   if constexpr (D == 2)
   {
-    pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf * mc, sm_count), 256, 0, s, P, xc, tA, mf, mc, 1, mc);
+    pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf, mc, 1), dim3(32, 8), 0, s, P, xc, tA, mf, mc, 1, mc);
     check_launch("prolong_pass0");
     if (acc)
-      pdl_launch(prolong_pass_kernel<K, T, 1, true>, pass_grid(mf * mf, sm_count), 256, 0, s, P, tA, xf, mf, mf, 1, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 1, true>, pass_grid(mf, mf, 1), dim3(32, 8), 0, s, P, tA, xf, mf, mf, 1, mc);
     else
-      pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf * mf, sm_count), 256, 0, s, P, tA, xf, mf, mf, 1, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf, mf, 1), dim3(32, 8), 0, s, P, tA, xf, mf, mf, 1, mc);
     check_launch("prolong_pass1");
   }
   else
   {
-    pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf * mc * mc, sm_count), 256, 0, s, P, xc, tA, mf, mc, mc, mc);
+    pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf, mc, mc), dim3(32, 8), 0, s, P, xc, tA, mf, mc, mc, mc);
     check_launch("prolong_pass0");
-    pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf * mf * mc, sm_count), 256, 0, s, P, tA, tB, mf, mf, mc, mc);
+    pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf, mf, mc), dim3(32, 8), 0, s, P, tA, tB, mf, mf, mc, mc);
     check_launch("prolong_pass1");
     if (acc)
-      pdl_launch(prolong_pass_kernel<K, T, 2, true>, pass_grid(mf * mf * mf, sm_count), 256, 0, s, P, tB, xf, mf, mf, mf, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 2, true>, pass_grid(mf, mf, mf), dim3(32, 8), 0, s, P, tB, xf, mf, mf, mf, mc);
     else
-      pdl_launch(prolong_pass_kernel<K, T, 2, false>, pass_grid(mf * mf * mf, sm_count), 256, 0, s, P, tB, xf, mf, mf, mf, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 2, false>, pass_grid(mf, mf, mf), dim3(32, 8), 0, s, P, tB, xf, mf, mf, mf, mc);
     check_launch("prolong_pass2");
   }
 }
@@ -180,18 +170,18 @@ void launch_restrict(const ProlMats<T, K> &P, const T *rf, T *rc, int64_t mc, T 
   const int64_t mf = 2 * mc + 1;
   if constexpr (D == 2)
   {
-    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc * mf, sm_count), 256, 0, s, P, rf, tA, mc, mf, 1, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, 1), dim3(32, 8), 0, s, P, rf, tA, mc, mf, 1, mf);
     check_launch("restrict_pass0");
-    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc * mc, sm_count), 256, 0, s, P, tA, rc, mc, mc, 1, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, 1), dim3(32, 8), 0, s, P, tA, rc, mc, mc, 1, mf);
     check_launch("restrict_pass1");
   }
   else
   {
-    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc * mf * mf, sm_count), 256, 0, s, P, rf, tA, mc, mf, mf, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, mf), dim3(32, 8), 0, s, P, rf, tA, mc, mf, mf, mf);
     check_launch("restrict_pass0");
-    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc * mc * mf, sm_count), 256, 0, s, P, tA, tB, mc, mc, mf, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, mf), dim3(32, 8), 0, s, P, tA, tB, mc, mc, mf, mf);
     check_launch("restrict_pass1");
-    pdl_launch(restrict_pass_kernel<K, T, 2>, pass_grid(mc * mc * mc, sm_count), 256, 0, s, P, tB, rc, mc, mc, mc, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 2>, pass_grid(mc, mc, mc), dim3(32, 8), 0, s, P, tB, rc, mc, mc, mc, mf);
     check_launch("restrict_pass2");
   }
 }
