@@ -7,6 +7,7 @@
 #include "smoother_impl.cuh"
 #include "smoother_plane.cuh"
 #include "smoother_point.cuh"
+#include "smoother_pp.cuh"
 #include "transfer_impl.cuh"
 
 #define PMG_CAT2(a, b) a##b
@@ -51,6 +52,21 @@ void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, 
         launch_vp_smooth_plane<PMG_K, T, MODE_FUSED>(PM, a, s);
       else
         launch_vp_smooth_plane<PMG_K, T, MODE_BOUNDARY>(PM, a, s);
+      return;
+    }
+  }
+  if constexpr (D == 3 && (PMG_K == 3 || PMG_K == 4 || (PMG_K == 5 && sizeof(T) == 4)))
+  {
+    // degree 3, 4 (and 5 in f32): ping-pong layouts (smoother_pp.cuh) unless
+    // the in-place line kernel is selected. Measured (profiles/r01): +6..11%
+    // at k = 3, 4; at k = 5 f64 and k >= 6 the second work buffer costs
+    // resident CTAs and the in-place kernel wins.
+    if (impl != SMOOTHER_IMPL_LINE && (mode == MODE_FUSED || mode == MODE_BOUNDARY))
+    {
+      if (mode == MODE_FUSED)
+        launch_vp_smooth_pp<PMG_K, T, MODE_FUSED>(PM, a, s);
+      else
+        launch_vp_smooth_pp<PMG_K, T, MODE_BOUNDARY>(PM, a, s);
       return;
     }
   }
