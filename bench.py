@@ -180,6 +180,19 @@ def run_reference_arm(args):
     print(json.dumps(out), flush=True)
 
 
+def smoother_kernel_name(args):
+    """The kernel organisation pmg_smooth dispatches to (instantiate.cuh)."""
+    if args.variant not in ("fused", "boundary"):
+        return "vp_smooth_kernel"
+    if args.degree == 1:
+        return "vp_point_kernel"
+    if args.dim == 3 and args.degree == 2:
+        return "vp_smooth_plane_kernel"
+    if args.dim == 3 and (args.degree in (3, 4) or (args.degree == 5 and args.dtype == "f32")):
+        return "vp_smooth_pp_kernel"
+    return "vp_smooth_kernel"
+
+
 def metric_name(args):
     return f"DoF/s per smoother step ({args.variant} vertex-patch, {args.dtype})"
 
@@ -359,7 +372,7 @@ def main():
         "frac": alg_bytes / launch_s / 1e9 / hbm_peak, "traffic": traffic,
         "traffic_note": "DRAM read+write bytes per step from ncu --set full (profiles/ncu_summary.json; "
                         "cold L2, per-colour launch x colours)",
-        "kernel": "vp_smooth_kernel (one launch per colour, summed over the 2^d colours)",
+        "kernel": smoother_kernel_name(args) + " (one launch per colour, summed over the 2^d colours)",
         "algorithmic_bytes_per_step": alg_bytes,
         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
     }

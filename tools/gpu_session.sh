@@ -45,9 +45,12 @@ if has launches; then
   echo "launches exit $?" >> "$OUT/status.txt"
 fi
 if has full; then
-  for cfg in "3 2 6 f64" "3 4 7 f64" "3 7 6 f64" "3 4 7 f32"; do
+  # the headline config: all 8 colour launches of one step (bench roofline.traffic)
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:vp_ -s 16 -c 8 \
+    -o "$OUT/smooth_d3k2L6f64" python tools/prof_target.py 3 2 6 f64 fused 3 > "$OUT/ncu_c2.log" 2>&1
+  for cfg in "3 1 9 f64" "3 4 7 f64" "3 7 6 f64" "3 4 7 f32"; do
     set -- $cfg
-    timeout 600 ncu --set full --clock-control none --import-source on -k regex:vp_smooth -s 8 -c 1 \
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:vp_ -s 8 -c 1 \
       -o "$OUT/smooth_d$1k$2L$3$4" python tools/prof_target.py $1 $2 $3 $4 fused 2 > "$OUT/ncu_d$1k$2$4.log" 2>&1
   done
   echo "full exit $?" >> "$OUT/status.txt"
