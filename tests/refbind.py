@@ -139,6 +139,19 @@ class RefMg:
         return st, x, it.value, hist[: it.value + 1].copy()
 
 
+def gmres(ref64, ref32, mixed, b, tol, restart=30, max_iterations=200):
+    """pmg_ref::gmres with the reference's V-cycle preconditioner
+    (krylov.cpp:24-171): mixed -> one f32 V-cycle of ref32, else f64 of ref64."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros_like(b)
+    it = ctypes.c_int()
+    hist = np.full(max_iterations + 8, np.nan)
+    st = lib().ref_gmres(ref64.h, ref32.h if ref32 is not None else ref64.h, int(mixed), P(b), P(x), tol,
+                         restart, max_iterations, ctypes.byref(it), P(hist), len(hist))
+    assert st == 0
+    return x, it.value, hist[: lib().ref_last_history_len()].copy()
+
+
 def compute_rhs(dim, k, level, kind):
     n = ((1 << level) * k - 1) ** dim
     b = np.zeros(n)
