@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -33,6 +34,18 @@ thread_local std::string g_last_error;
 void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 std::atomic<int> g_smoother_impl{SMOOTHER_IMPL_AUTO};
+
+// levels with at most this many plane tiles run their 2^d colours as one
+// persistent sweep under the default implementation (PMG_SWEEP_AUTO_TILES
+// overrides; measurement knob)
+int64_t sweep_auto_tiles()
+{
+  static const int64_t v = [] {
+    const char *e = std::getenv("PMG_SWEEP_AUTO_TILES");
+    return e ? std::atoll(e) : int64_t(0);
+  }();
+  return v;
+}
 int smoother_impl_choice() { return g_smoother_impl.load(std::memory_order_relaxed); }
 
 void check_launch(const char *what)
@@ -353,14 +366,26 @@ template <typename T>
 bool sweep_impl(pmg_level_s *l, int variant, T *x, const T *b, cudaStream_t s)
 {
   const int impl = smoother_impl_choice();
-  // measured slower than per-colour launches (per-tile ticket / counter
-  // traffic outweighs the saved tails): opt-in only
-  if (impl != SMOOTHER_IMPL_SWEEP || l->S.dim != 3 ||
+  // measured slower than per-colour launches on large levels (per-tile
+  // ticket / counter traffic outweighs the saved tails):
+  // opt-in, or automatic on levels of at most sweep_auto_tiles() tiles
+  if (!(impl == SMOOTHER_IMPL_SWEEP || impl == SMOOTHER_IMPL_AUTO) || l->S.dim != 3 ||
       !(variant == PMG_FUSED || variant == PMG_BOUNDARY))
     return false;
   const auto &kt = ktab<T>(l);
   if (!kt.sweep || kt.sweep_pb <= 0)
     return false;
+  if (impl == SMOOTHER_IMPL_AUTO)
+  {
+    int64_t tiles = 0;
+    for (int c = 0; c < (1 << l->S.dim); ++c)
+    {
+      const ColorArgs<T> a = color_args<T>(l, c, x, b);
+      tiles += static_cast<int64_t>((a.np[0] + kt.sweep_pb - 1) / kt.sweep_pb) * a.np[1] * a.np[2];
+    }
+    if (tiles > sweep_auto_tiles())
+      return false;
+  }
   SweepArgs<T> sw{};
   sw.ncolors = 1 << l->S.dim;
   sw.nv = l->S.n + 1;
