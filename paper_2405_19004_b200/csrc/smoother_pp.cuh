@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
 {
   pdl_prologue();
   using C = PPCfg<K, T>;
-  constexpr int NC = C::NC, NI = C::NI, PB = C::PB, NT = C::NT, UW = C::UW, BW = C::BW;
+  constexpr int NC = C::NC, NI = C::NI, PB = C::PB, UW = C::UW, BW = C::BW;
   constexpr int A_ = 0, B_ = 1, C_ = 2, D_ = 3, E_ = 4, F_ = 5, G_ = 6;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *U = reinterpret_cast<T *>(smem_raw);  // [PB][UW]

@@ -14,6 +14,8 @@
 // prolongation pass can accumulate into x (the V-cycle's x += P x_c).
 #pragma once
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace pmgb
@@ -128,10 +130,122 @@ __global__ void __launch_bounds__(256)
   out[(i2 * e1 + i1) * e0 + i0] = s;
 }
 
+// PMG_TRANSFER_PASSES=1 selects the separate 1D passes (A/B measurement)
+inline bool use_fused_transfer()
+{
+  static const bool v = [] {
+    const char *e = std::getenv("PMG_TRANSFER_PASSES");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}
+
 inline dim3 pass_grid(int64_t e0, int64_t e1, int64_t e2)
 {
   return dim3(static_cast<unsigned>((e0 + 31) / 32), static_cast<unsigned>((e1 + 7) / 8),
               static_cast<unsigned>(e2));
+}
+
+// ---------------------------------------------------------------------------
+// 3D prolongation in one kernel: CTA = CX x CY coarse cells of one z-cell.
+// The (K+1)^3-node coarse block of the tile is staged once, then the three 1D
+// passes run in shared memory (x: coarse rows -> fine columns, y, z) and the
+// (2K)^3 fine nodes per cell are written (or accumulated) straight to x_f.
+// Traffic: x_c once (+ halo) and x_f once (twice with accumulation), against
+// ~3.5 N words for the three separate passes; one launch instead of three.
+// ---------------------------------------------------------------------------
+template <int K>
+struct Prol3Cfg
+{
+  static constexpr int CX = (32 / (2 * K)) > 0 ? 32 / (2 * K) : 1;
+  static constexpr int CY = (8 / (2 * K)) > 0 ? 8 / (2 * K) : 1;
+  static constexpr int FX = 2 * K * CX, FY = 2 * K * CY;
+  static constexpr int QX = CX * K + 1, QY = CY * K + 1, QZ = K + 1;  // coarse block
+  static constexpr int NT = 32 * FY;
+};
+
+template <int K, typename T, bool ACC>
+__global__ void __launch_bounds__(Prol3Cfg<K>::NT)
+    prolong3d_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ xc, T *__restrict__ xf,
+                     int mc, int nc)
+{
+  pdl_prologue();
+  using C = Prol3Cfg<K>;
+  constexpr int CX = C::CX, CY = C::CY, FX = C::FX, FY = C::FY, QX = C::QX, QY = C::QY, QZ = C::QZ, NT = C::NT;
+  __shared__ T Ps[2 * K + 1][K + 1];
+  __shared__ T Cs[QZ][QY][QX];
+  __shared__ T T1[QZ][QY][FX];
+  __shared__ T T2[QZ][FY][FX];
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int e = tid; e < (2 * K + 1) * (K + 1); e += NT)
+    (&Ps[0][0])[e] = (&P.P[0][0])[e];
+  const int cx0 = blockIdx.x * CX, cy0 = blockIdx.y * CY, cz = blockIdx.z;
+  const int64_t mc2 = static_cast<int64_t>(mc) * mc;
+  // coarse lattice q = cK + t (1-based; 0 and mc+1 are the Dirichlet boundary)
+  for (int e = tid; e < QZ * QY * QX; e += NT)
+  {
+    const int iz = e / (QY * QX), r = e - iz * (QY * QX);
+    const int iy = r / QX, ix = r - iy * QX;
+    const int qx = cx0 * K + ix, qy = cy0 * K + iy, qz = cz * K + iz;
+    T v = T(0);
+    if (qx >= 1 && qx <= mc && qy >= 1 && qy <= mc && qz >= 1 && qz <= mc)
+      v = __ldg(xc + (qz - 1) * mc2 + static_cast<int64_t>(qy - 1) * mc + (qx - 1));
+    Cs[iz][iy][ix] = v;
+  }
+  __syncthreads();
+  // x: fine column fx = 2K c + (r - 1) of the tile, r = 1..2K
+  for (int e = tid; e < QZ * QY * FX; e += NT)
+  {
+    const int iz = e / (QY * FX), rr = e - iz * (QY * FX);
+    const int iy = rr / FX, fx = rr - iy * FX;
+    const int c = fx / (2 * K), r = fx - 2 * K * c + 1;
+    T s = T(0);
+#pragma unroll
+    for (int t = 0; t <= K; ++t)
+      s = fma(Ps[r][t], Cs[iz][iy][c * K + t], s);
+    T1[iz][iy][fx] = s;
+  }
+  __syncthreads();
+  const int fx = threadIdx.x, fy = threadIdx.y;
+  const int cyl = fy / (2 * K), ry = fy - 2 * K * cyl + 1;
+  if (fx < FX)
+  {
+#pragma unroll
+    for (int iz = 0; iz < QZ; ++iz)
+    {
+      T s = T(0);
+#pragma unroll
+      for (int t = 0; t <= K; ++t)
+        s = fma(Ps[ry][t], T1[iz][cyl * K + t][fx], s);
+      T2[iz][fy][fx] = s;
+    }
+  }
+  __syncthreads();
+  if (fx >= FX)
+    return;
+  const int cxl = fx / (2 * K), rx = fx - 2 * K * cxl + 1;
+  const int mf = 2 * mc + 1;
+  const int px = 2 * (cx0 + cxl) * K + rx, py = 2 * (cy0 + cyl) * K + ry;  // fine lattice
+  if (cx0 + cxl >= nc || cy0 + cyl >= nc || px > mf || py > mf)
+    return;
+  const int64_t mf2 = static_cast<int64_t>(mf) * mf;
+  T *o = xf + static_cast<int64_t>(py - 1) * mf + (px - 1);
+#pragma unroll
+  for (int rz = 1; rz <= 2 * K; ++rz)
+  {
+    const int pz = 2 * cz * K + rz;
+    if (pz > mf)
+      break;
+    T s = T(0);
+#pragma unroll
+    for (int t = 0; t <= K; ++t)
+      s = fma(Ps[rz][t], T2[t][fy][fx], s);
+    T *op = o + (pz - 1) * mf2;
+    if constexpr (ACC)
+      *op += s;
+    else
+      *op = s;
+  }
 }
 
 template <int D, int K, typename T>
@@ -148,6 +262,17 @@ void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, in
     else
       pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf, mf, 1), dim3(32, 8), 0, s, P, tA, xf, mf, mf, 1, mc);
     check_launch("prolong_pass1");
+  }
+  else if (use_fused_transfer())
+  {
+    using C = Prol3Cfg<K>;
+    const int nc = static_cast<int>((mc + 1) / K);  // coarse cells per direction
+    const dim3 grid((nc + C::CX - 1) / C::CX, (nc + C::CY - 1) / C::CY, nc);
+    if (acc)
+      pdl_launch(prolong3d_kernel<K, T, true>, grid, dim3(32, C::FY), 0, s, P, xc, xf, static_cast<int>(mc), nc);
+    else
+      pdl_launch(prolong3d_kernel<K, T, false>, grid, dim3(32, C::FY), 0, s, P, xc, xf, static_cast<int>(mc), nc);
+    check_launch("prolong3d_kernel");
   }
   else
   {
