@@ -151,6 +151,14 @@ int pmg_compute_rhs_host(int dim, int degree, int level, int kind, double *out);
 /* ~ l2_error(level, x, u)   operator.hpp:62-64 for u = prod sin(pi x_a). */
 int pmg_l2_error_sin_host(int dim, int degree, int level, const double *x, double *out);
 
+/* Device versions (same kinds / quadrature; no reference counterpart on the
+ * device): b (device, the level's dtype, N entries) = compute_rhs of the
+ * level, formed as the tensor power of the 1D load vector (exact on the
+ * uniform level); l2_error evaluates u_h - u pointwise at the (k+2)^d Gauss
+ * points of every cell (x: device, the level's dtype). */
+int pmg_compute_rhs(pmg_level h, int kind, void *b, void *stream);
+int pmg_l2_error_sin(pmg_level h, const void *x, double *out, void *stream);
+
 /* ---- mixed precision / Krylov (krylov.hpp:30-39) -------------------------
  * Right-preconditioned GMRES(restart) in f64 on the device with the V-cycle
  * of `prec` (an f32 context: mixed precision; an f64 context: double) as the

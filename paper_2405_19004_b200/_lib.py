@@ -58,6 +58,8 @@ SIGNATURES = [
     ("pmg_host_level_setup", _i, [_i, _i, _i] + [_pd] * 9 + [_pi]),
     ("pmg_launch_count", _i64, []),
     ("pmg_set_smoother_impl", _i, [_i]),
+    ("pmg_compute_rhs", _i, [_vp, _i, _vp, _vp]),
+    ("pmg_l2_error_sin", _i, [_vp, _vp, _pd, _vp]),
     ("pmg_get_smoother_impl", _i, []),
 ]
 

@@ -670,6 +670,14 @@ int mg_levels(pmg_mg h) { return static_cast<int>(h->levels.size()); }
 pmg_level mg_level_ptr(pmg_mg h, int li) { return h->levels[li]; }
 int64_t level_total(pmg_level l) { return l->S.N; }
 int level_sm_count(pmg_level l) { return l->sm_count; }
+void level_params(pmg_level l, int *dim, int *k, int *level, int *dtype, int *device)
+{
+  *dim = l->S.dim;
+  *k = l->S.k;
+  *level = l->S.level;
+  *dtype = l->dtype;
+  *device = l->device;
+}
 GmresWork &mg_gmres_work(pmg_mg h) { return h->gmres; }
 
 void mg_apply_finest_op(pmg_mg h, const double *x, double *y, cudaStream_t s)

@@ -94,6 +94,7 @@ int mg_levels(pmg_mg h);
 pmg_level mg_level_ptr(pmg_mg h, int li);
 int64_t level_total(pmg_level l);
 int level_sm_count(pmg_level l);
+void level_params(pmg_level l, int *dim, int *k, int *level, int *dtype, int *device);
 GmresWork &mg_gmres_work(pmg_mg h);
 void mg_apply_finest_op(pmg_mg h, const double *x, double *y, cudaStream_t s);
 void mg_residual_finest(pmg_mg h, const double *x, const double *b, double *r, cudaStream_t s);

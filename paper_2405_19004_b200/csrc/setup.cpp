@@ -455,9 +455,6 @@ LevelSetup make_level_setup(int dim, int k, int level)
   return s;
 }
 
-namespace
-{
-
 // 1D load vector of g over the level lattice interior: sum over cells of
 // sum_q w h g(x_q) phi_t(x_q), k+2 Gauss points.
 std::vector<double> rhs_1d(int k, int n, bool sine)
@@ -478,8 +475,6 @@ std::vector<double> rhs_1d(int k, int n, bool sine)
     }
   return std::vector<double>(lat.begin() + 1, lat.end() - 1);
 }
-
-}  // namespace
 
 std::vector<double> compute_rhs(int dim, int k, int level, int kind)
 {

@@ -68,6 +68,10 @@ void generalized_eigen(const Dense &A, const Dense &M, Dense &S, std::vector<dou
 // b_i = int f phi_i with (k+2)-point Gauss per direction; kind 0: f = 1,
 // kind 1: f = d pi^2 prod sin(pi x_a).
 std::vector<double> compute_rhs(int dim, int k, int level, int kind);
+// 1D factor of compute_rhs: the load vector of g = 1 or sin(pi x) on the
+// interior lattice (the d-D right-hand side is its tensor power times 1 or
+// d pi^2)
+std::vector<double> rhs_1d(int k, int n, bool sine);
 double l2_error_sin(int dim, int k, int level, const double *x);
 
 }  // namespace pmgb

@@ -36,7 +36,7 @@ __all__ = [
     "MultigridContext", "make_multigrid_context", "SmootherVariant", "smooth", "smooth_color", "smooth_color_slab",
     "apply_laplacian", "compute_residual", "prolongate", "restrict_vector", "v_cycle",
     "full_multigrid", "FmgStats", "vector_norm", "compute_rhs", "l2_error", "gmres", "SolveStats",
-    "DivergenceError", "set_smoother_impl", "get_smoother_impl",
+    "DivergenceError", "set_smoother_impl", "get_smoother_impl", "compute_rhs_device",
 ]
 
 _SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2, "sweep": 3}
@@ -510,10 +510,30 @@ def compute_rhs(level: CartesianLevel, f: str = "one") -> np.ndarray:
     return out
 
 
-def l2_error(level: CartesianLevel, x, u_exact: str = "sin") -> float:
-    """L2 error against u = prod sin(pi x_a) (operator.hpp:62-64)."""
+def compute_rhs_device(ctx: LevelContext, f: str, out) -> None:
+    """compute_rhs on the device into `out` (a CUDA tensor of the level's
+    dtype): the tensor power of the 1D load vector, exact on the uniform
+    level (operator.cpp:283-344 computes the same integrals cell by cell)."""
+    kinds = {"one": 0, "sin": 1}
+    if f not in kinds:
+        raise ValueError("compute_rhs: f must be 'one' or 'sin'")
+    a = _Arr(out, ctx.level.total_dofs, ctx._code, "b", True)
+    check(_lib.load().pmg_compute_rhs(ctx.handle, kinds[f], a.ptr, _stream([out])), "compute_rhs")
+
+
+def l2_error(level, x, u_exact: str = "sin") -> float:
+    """L2 error against u = prod sin(pi x_a) (operator.hpp:62-64). With a
+    LevelContext and a CUDA tensor the (k+2)^d-point Gauss rule runs on the
+    device (pointwise, no cancellation); otherwise on the host."""
     if u_exact != "sin":
         raise ValueError("l2_error: only u = prod sin(pi x) is provided")
+    if isinstance(level, LevelContext) and _is_torch(x) and x.is_cuda:
+        a = _Arr(x, level.level.total_dofs, level._code, "x", False)
+        out = ctypes.c_double()
+        check(_lib.load().pmg_l2_error_sin(level.handle, a.ptr, ctypes.byref(out), _stream([x])), "l2_error")
+        return out.value
+    if isinstance(level, LevelContext):
+        level = level.level
     xh = x.detach().cpu().numpy() if _is_torch(x) else np.ascontiguousarray(x, dtype=np.float64)
     xh = np.ascontiguousarray(xh, dtype=np.float64)
     if xh.size != level.total_dofs:

@@ -7,6 +7,8 @@ relative to ||b||, SURVEY.md §7 "FP32 parity definition"); FMG iteration
 counts identical at a 1e-8 reduction.
 """
 
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -22,6 +24,10 @@ CASES = [
     (2, 1, 5), (2, 2, 6), (2, 3, 4), (2, 4, 4), (2, 5, 3), (2, 6, 3), (2, 7, 3),
     (3, 1, 4), (3, 2, 4), (3, 3, 3), (3, 4, 3), (3, 5, 2), (3, 6, 2), (3, 7, 2),
 ]
+
+
+def ctypes_double():
+    return ctypes.c_double()
 
 
 def rel(a, b):
@@ -331,3 +337,31 @@ def test_gmres_vs_reference(pmg, cuda, case, mode):
     htol = 1e-9 if mode == "double" else 1e-4
     assert np.allclose(h, hr, rtol=htol, atol=htol * hr[0]), (h, hr)
     assert rel(xd.cpu().numpy(), xr) < (1e-9 if mode == "double" else 1e-6)
+
+
+# Device right-hand side and L2 error against the reference's compute_rhs and
+# the host quadrature (operator.cpp:283-411): rhs relative 1e-14 (f64), L2
+# error relative 1e-9 (both evaluate u_h - u pointwise at the same Gauss points).
+@pytest.mark.parametrize("case", [(2, 1, 5), (2, 4, 4), (3, 1, 4), (3, 2, 4), (3, 5, 2), (3, 7, 2)],
+                         ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")
+def test_device_rhs_and_l2(pmg, cuda, case):
+    dim, k, L = case
+    ctx = pmg.make_multigrid_context(dim, k, L, dtype=np.float64)
+    lev = ctx.levels[-1]
+    for f, kind in [("one", 0), ("sin", 1)]:
+        want = refbind.compute_rhs(dim, k, L, kind)
+        got = cuda.empty(want.size, dtype=cuda.float64, device="cuda")
+        pmg.compute_rhs_device(lev, f, got)
+        assert rel(got.cpu().numpy(), want) < 1e-14
+    # a discrete solution-like field: the FMG-free sine interpolant plus noise
+    x = np.random.default_rng(3).uniform(-1e-3, 1e-3, lev.level.total_dofs)
+    e_host = pmg.l2_error(lev.level, x)
+    e_dev = pmg.l2_error(lev, dev(cuda, x))
+    e_ref = ctypes_double()
+    assert refbind.lib().ref_l2_error_sin(dim, k, L, refbind.P(x), ctypes.byref(e_ref)) == 0
+    assert abs(e_dev - e_host) <= 1e-9 * e_host, (e_dev, e_host)
+    assert abs(e_dev - e_ref.value) <= 1e-9 * e_ref.value, (e_dev, e_ref.value)
+    ctx32 = pmg.make_multigrid_context(dim, k, L, dtype=np.float32)
+    got32 = cuda.empty(lev.level.total_dofs, dtype=cuda.float32, device="cuda")
+    pmg.compute_rhs_device(ctx32.levels[-1], "sin", got32)
+    assert rel(got32.cpu().numpy(), refbind.compute_rhs(dim, k, L, 1)) < 1e-6

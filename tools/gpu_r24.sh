@@ -1,4 +1,4 @@
-O=gpurun_out/r24; mkdir -p $O
+O=gpurun_out/r25; mkdir -p $O
 timeout 600 python -m pytest tests -m gpu -x -q -k "transfer or prolong or restrict or vcycle or v_cycle or fmg or gmres" > $O/pytest.log 2>&1; echo "pytest $?" >> $O/status.txt
 for v in 1 0; do
 echo "== passes=$v" >> $O/ab.log
