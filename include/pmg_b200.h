@@ -185,6 +185,23 @@ int pmg_host_level_setup(int dim, int degree, int level, double *S, double *lamb
                          double *cell_mass, double *cell_stiffness, double *band_mass,
                          double *band_stiff, int *eo_perm);
 
+/* Slab domain decomposition (3D, along direction 2; paper_2405_19004_b200/dd.py).
+ * Device arrays hold the GLOBAL dof planes [zoff, zoff + nplanes) of a level
+ * vector (m*m words per plane, the reference layout otherwise). Each call
+ * computes only the requested global output planes and fails with
+ * PMG_ERR_INVALID if the slab does not hold the planes they depend on. Every
+ * output value is computed exactly as by the full-domain call, so slabs
+ * reproduce the single-GPU V-cycle bitwise.
+ *   residual r = b - A x on planes [p0, p1)            (multigrid.cpp:268-276)
+ *   restriction to coarse planes [q0, q1)              (multigrid.cpp:162-248)
+ *   prolongation (accumulate != 0: +=) on fine [f0, f1) (multigrid.cpp:71-160) */
+int pmg_compute_residual_slab(pmg_level h, const void *x, const void *b, void *r, int64_t zoff, int64_t nplanes,
+                              int64_t p0, int64_t p1, void *stream);
+int pmg_restrict_slab(pmg_level coarse, pmg_level fine, const void *rf, int64_t zoff_f, int64_t np_f, void *rc,
+                      int64_t zoff_c, int64_t np_c, int64_t q0, int64_t q1, void *stream);
+int pmg_prolongate_slab(pmg_level coarse, pmg_level fine, const void *xc, int64_t zoff_c, int64_t np_c, void *xf,
+                        int64_t zoff_f, int64_t np_f, int64_t f0, int64_t f1, int accumulate, void *stream);
+
 /* Number of kernel launches issued by this library since load (counter). */
 int64_t pmg_launch_count(void);
 

@@ -59,6 +59,9 @@ SIGNATURES = [
     ("pmg_launch_count", _i64, []),
     ("pmg_set_smoother_impl", _i, [_i]),
     ("pmg_compute_rhs", _i, [_vp, _i, _vp, _vp]),
+    ("pmg_compute_residual_slab", _i, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
+    ("pmg_restrict_slab", _i, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),
+    ("pmg_prolongate_slab", _i, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i, _vp]),
     ("pmg_l2_error_sin", _i, [_vp, _vp, _pd, _vp]),
     ("pmg_get_smoother_impl", _i, []),
 ]

@@ -18,6 +18,7 @@
 #include "../../include/pmg_b200.h"
 #include "blas.cuh"
 #include "dispatch.hpp"
+#include "transfer_impl.cuh"
 #include "naive.cuh"
 #include "setup.hpp"
 #include "capi_internal.hpp"
@@ -704,6 +705,30 @@ void mg_vcycle_f64(pmg_mg h, int li, double *x, const double *b, cudaStream_t s)
 
 }  // namespace pmgb
 
+// ---- slab entry points (3D slab domain decomposition, dd.py) ------------------
+namespace
+{
+void require_planes(const char *what, int64_t zoff, int64_t np, int64_t lo, int64_t hi, int64_t m)
+{
+  // global planes [lo, hi) clipped to the domain must lie in [zoff, zoff + np)
+  lo = std::max<int64_t>(lo, 0);
+  hi = std::min<int64_t>(hi, m);
+  if (lo < hi && (lo < zoff || hi > zoff + np))
+    throw InvalidArg(std::string(what) + ": slab does not hold the planes the requested outputs depend on");
+}
+
+template <typename T>
+const T *shift(const void *p, int64_t zoff, int64_t plane)
+{
+  return static_cast<const T *>(p) - zoff * plane;
+}
+template <typename T>
+T *shift(void *p, int64_t zoff, int64_t plane)
+{
+  return static_cast<T *>(p) - zoff * plane;
+}
+}  // namespace
+
 extern "C" {
 
 const char *pmg_last_error(void) { return g_last_error.c_str(); }
@@ -892,6 +917,74 @@ int pmg_compute_residual(pmg_level h, const void *x, const void *b, void *r, voi
     PMG_DISPATCH_T(h, ktab<T>(h).level_op(h->band_mats.data(), static_cast<const T *>(x),
                                           static_cast<const T *>(b), static_cast<T *>(r), h->S.m,
                                           h->sm_count, as_stream(stream)));
+  });
+}
+
+
+int pmg_compute_residual_slab(pmg_level h, const void *x, const void *b, void *r, int64_t zoff, int64_t nplanes,
+                              int64_t p0, int64_t p1, void *stream)
+{
+  return guard([&] {
+    require_level(h);
+    if (h->S.dim != 3)
+      throw InvalidArg("compute_residual_slab: dim 3 only");
+    if (!x || !b || !r || nplanes < 0 || p0 < 0 || p1 > h->S.m || p0 > p1)
+      throw InvalidArg("compute_residual_slab: invalid arguments");
+    require_planes("compute_residual_slab", zoff, nplanes, p0 - h->S.k, p1 + h->S.k, h->S.m);
+    require_planes("compute_residual_slab", zoff, nplanes, p0, p1, h->S.m);
+    DeviceGuard dg(h->device);
+    const int64_t pl = h->S.m * h->S.m;
+    PMG_DISPATCH_T(h, ktab<T>(h).level_op_range(h->band_mats.data(), shift<T>(x, zoff, pl), shift<T>(b, zoff, pl),
+                                                shift<T>(r, zoff, pl), h->S.m, p0, p1, h->sm_count,
+                                                as_stream(stream)));
+  });
+}
+
+int pmg_restrict_slab(pmg_level c, pmg_level f, const void *rf, int64_t zoff_f, int64_t np_f, void *rc,
+                      int64_t zoff_c, int64_t np_c, int64_t q0, int64_t q1, void *stream)
+{
+  return guard([&] {
+    check_pair(c, f, "restrict_slab");
+    if (f->S.dim != 3)
+      throw InvalidArg("restrict_slab: dim 3 only");
+    if (!rf || !rc || q0 < 0 || q1 > c->S.m || q0 > q1)
+      throw InvalidArg("restrict_slab: invalid arguments");
+    int64_t pz0 = 0, pz1 = 0;
+    restrict_slab_fine_range(f->S.k, c->S.m, q0, q1, pz0, pz1);
+    require_planes("restrict_slab (fine)", zoff_f, np_f, pz0, pz1, f->S.m);
+    require_planes("restrict_slab (coarse)", zoff_c, np_c, q0, q1, c->S.m);
+    DeviceGuard dg(f->device);
+    const int64_t mc = c->S.m, mf = f->S.m, np = std::max<int64_t>(pz1 - pz0, 0);
+    PMG_DISPATCH_T(f, {
+      f->tA.ensure(static_cast<size_t>(mc * mf * np) * sizeof(T) + sizeof(T));
+      f->tB.ensure(static_cast<size_t>(mc * mc * np) * sizeof(T) + sizeof(T));
+      ktab<T>(f).restrict_slab(f->prol_mats.data(), shift<T>(rf, zoff_f, mf * mf), shift<T>(rc, zoff_c, mc * mc),
+                               mc, q0, q1, f->tA.as<T>() - pz0 * mc * mf, f->tB.as<T>() - pz0 * mc * mc,
+                               as_stream(stream));
+    });
+  });
+}
+
+int pmg_prolongate_slab(pmg_level c, pmg_level f, const void *xc, int64_t zoff_c, int64_t np_c, void *xf,
+                        int64_t zoff_f, int64_t np_f, int64_t f0, int64_t f1, int accumulate, void *stream)
+{
+  return guard([&] {
+    check_pair(c, f, "prolongate_slab");
+    if (f->S.dim != 3)
+      throw InvalidArg("prolongate_slab: dim 3 only");
+    if (!xc || !xf || f0 < 0 || f1 > f->S.m || f0 > f1)
+      throw InvalidArg("prolongate_slab: invalid arguments");
+    const int64_t K = f->S.k, mc = c->S.m, mf = f->S.m;
+    if (f0 < f1)
+    {
+      const int64_t cz0 = f0 / (2 * K), cz1 = (f1 - 1) / (2 * K);  // coarse cells
+      require_planes("prolongate_slab (coarse)", zoff_c, np_c, cz0 * K - 1, cz1 * K + K, mc);
+    }
+    require_planes("prolongate_slab (fine)", zoff_f, np_f, f0, f1, mf);
+    DeviceGuard dg(f->device);
+    PMG_DISPATCH_T(f, ktab<T>(f).prolongate_slab(f->prol_mats.data(), shift<T>(xc, zoff_c, mc * mc),
+                                                 shift<T>(xf, zoff_f, mf * mf), accumulate != 0, mc, f0, f1,
+                                                 as_stream(stream)));
   });
 }
 

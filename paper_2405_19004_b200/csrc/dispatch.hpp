@@ -19,6 +19,13 @@ struct KernelTable
   // B: BandMats<T,K>*; b == nullptr -> y = A x, else y = b - A x
   void (*level_op)(const void *B, const T *x, const T *b, T *y, int64_t m, int sm_count,
                    cudaStream_t s) = nullptr;
+  // slab versions (3D): global-plane bases, output planes [z0, z1)
+  void (*level_op_range)(const void *B, const T *x, const T *b, T *y, int64_t m, int64_t z0, int64_t z1,
+                         int sm_count, cudaStream_t s) = nullptr;
+  void (*prolongate_slab)(const void *P, const T *xc, T *xf, bool acc, int64_t mc, int64_t f0, int64_t f1,
+                          cudaStream_t s) = nullptr;
+  void (*restrict_slab)(const void *P, const T *rf, T *rc, int64_t mc, int64_t q0, int64_t q1, T *tA, T *tB,
+                        cudaStream_t s) = nullptr;
   // P: ProlMats<T,K>*
   void (*prolongate)(const void *P, const T *xc, T *xf, bool acc, int64_t mc, T *tA, T *tB,
                      int sm_count, cudaStream_t s) = nullptr;

@@ -113,6 +113,26 @@ void rest_entry(const void *P, const T *rf, T *rc, int64_t mc, T *tA, T *tB, int
 }
 
 template <int D, typename T>
+void op_range_entry(const void *B, const T *x, const T *b, T *y, int64_t m, int64_t z0, int64_t z1, int sm_count,
+                    cudaStream_t s)
+{
+  launch_level_op<D, PMG_K, T>(*static_cast<const BandMats<T, PMG_K> *>(B), x, b, y, m, sm_count, s, z0, z1);
+}
+
+template <typename T>
+void prol_slab_entry(const void *P, const T *xc, T *xf, bool acc, int64_t mc, int64_t f0, int64_t f1, cudaStream_t s)
+{
+  launch_prolongate_slab<PMG_K, T>(*static_cast<const ProlMats<T, PMG_K> *>(P), xc, xf, acc, mc, f0, f1, s);
+}
+
+template <typename T>
+void rest_slab_entry(const void *P, const T *rf, T *rc, int64_t mc, int64_t q0, int64_t q1, T *tA, T *tB,
+                     cudaStream_t s)
+{
+  launch_restrict_slab<PMG_K, T>(*static_cast<const ProlMats<T, PMG_K> *>(P), rf, rc, mc, q0, q1, tA, tB, s);
+}
+
+template <int D, typename T>
 KernelTable<T> make_table()
 {
   KernelTable<T> t;
@@ -120,6 +140,12 @@ KernelTable<T> make_table()
   t.sweep = &sweep_entry<D, T>;
   t.sweep_pb = PMG_K == 2 ? PlaneCfg<2, T>::PB : 0;
   t.level_op = &op_entry<D, T>;
+  if constexpr (D == 3)
+  {
+    t.level_op_range = &op_range_entry<D, T>;
+    t.prolongate_slab = &prol_slab_entry<T>;
+    t.restrict_slab = &rest_slab_entry<T>;
+  }
   t.prolongate = &prol_entry<D, T>;
   t.restrict_ = &rest_entry<D, T>;
   t.smooth_smem = sm_smem_bytes<D, PMG_K, T>();

@@ -79,7 +79,8 @@ constexpr int op3d_minb()
 template <int K, typename T, bool RESID>
 __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
     level_op3d_kernel(const __grid_constant__ BandMats<T, K> B, const T *__restrict__ x,
-                      const T *__restrict__ b, T *__restrict__ y, int64_t m, int zchunk)
+                      const T *__restrict__ b, T *__restrict__ y, int64_t m, int zchunk, int64_t zbeg,
+                      int64_t zend)
 {
   pdl_prologue();
   using C = Op3Cfg<K, T>;
@@ -102,8 +103,10 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
   }
   const int g0 = static_cast<int>(blockIdx.x) * TX;
   const int g1 = static_cast<int>(blockIdx.y) * TY;
-  const int64_t zs = static_cast<int64_t>(blockIdx.z) * zchunk;  // multiple of K
-  const int64_t ze = min(zs + zchunk, m);
+  // output planes [zbeg, zend) (x, b, y indexed by GLOBAL plane: slab callers
+  // pass bases shifted by their first plane); chunks start on multiples of K
+  const int64_t zs = (zbeg / K) * K + static_cast<int64_t>(blockIdx.z) * zchunk;  // multiple of K
+  const int64_t ze = min(zs + zchunk, zend);
   const int64_t m2 = m * m;
   // this thread's tile slots: in-plane offset and validity (fixed for all planes)
   int off[NLOAD];
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
     if constexpr (RESID)
     {
       const int64_t p = q - K;
-      const bool ok = out_ok && it >= 2 * K && p < ze;
+      const bool ok = out_ok && it >= 2 * K && p < ze && p >= zbeg;
       op_cp_async(Bv + (it % 3) * NT + tid, ok ? b + p * m2 + out_off : b, ok);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
         acc[jo] = fma(B.M[res][2 * K - jo], ws, acc[jo]);
       }
       const int64_t p_out = zs - 2 * K + it;
-      if (it >= 2 * K && p_out < ze && out_ok)
+      if (it >= 2 * K && p_out < ze && p_out >= zbeg && out_ok)
       {
         const int64_t idx = p_out * m2 + out_off;
         if constexpr (RESID)
@@ -380,8 +383,12 @@ __global__ void __launch_bounds__(128)
 
 template <int D, int K, typename T>
 void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int64_t m,
-                     int sm_count, cudaStream_t s)
+                     int sm_count, cudaStream_t s, int64_t zbeg = 0, int64_t zend = -1)
 {
+  if (zend < 0)
+    zend = m;
+  if (zend <= zbeg)
+    return;
   if constexpr (D == 3)
   {
     using C = Op3Cfg<K, T>;
@@ -390,12 +397,13 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
     const unsigned gy = static_cast<unsigned>((m + C::TY - 1) / C::TY);
     // z chunk (a multiple of K): enough CTAs for ~6 per SM, >= 4k planes to
     // bound the recomputed halo
+    const int64_t z0 = (zbeg / K) * K, span = zend - z0;
     int64_t want = static_cast<int64_t>(sm_count) * 6;
     int64_t nz = (want + gx * gy - 1) / (gx * gy);
-    int64_t zchunk = (m + nz - 1) / nz;
+    int64_t zchunk = (span + nz - 1) / nz;
     zchunk = std::max<int64_t>(zchunk, 4 * K);
     zchunk = (zchunk + K - 1) / K * K;
-    const unsigned gz = static_cast<unsigned>((m + zchunk - 1) / zchunk);
+    const unsigned gz = static_cast<unsigned>((span + zchunk - 1) / zchunk);
     auto kern = b ? level_op3d_kernel<K, T, true> : level_op3d_kernel<K, T, false>;
     static unsigned attr_mask[2] = {0, 0};
     if (first_on_device(attr_mask[b ? 1 : 0]))
@@ -406,7 +414,7 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
       check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
                  "cudaFuncSetAttribute(level_op3d carveout)");
     }
-    pdl_launch(kern, dim3(gx, gy, gz), C::NT, smem, s, B, x, b, y, m, static_cast<int>(zchunk));
+    pdl_launch(kern, dim3(gx, gy, gz), C::NT, smem, s, B, x, b, y, m, static_cast<int>(zchunk), zbeg, zend);
     check_launch("level_op3d_kernel");
   }
   else

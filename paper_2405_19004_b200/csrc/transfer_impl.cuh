@@ -51,7 +51,7 @@ __device__ __forceinline__ void pass_index(int64_t e0, int64_t e1, int64_t ie0, 
 template <int K, typename T, int DIR, bool ACC>
 __global__ void __launch_bounds__(256)
     prolong_pass_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ in,
-                        T *__restrict__ out, int64_t e0, int64_t e1, int64_t e2, int64_t mc)
+                        T *__restrict__ out, int64_t e0, int64_t e1, int64_t e2, int64_t mc, int64_t z0)
 {
   pdl_prologue();
   __shared__ T Ps[2 * K + 1][K + 1];
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
   const int64_t i1 = static_cast<int64_t>(blockIdx.y) * 8 + threadIdx.y;
-  const int64_t i2 = blockIdx.z;
+  const int64_t i2 = z0 + blockIdx.z;  // global plane (slab callers shift their bases)
   if (i0 >= e0 || i1 >= e1)
     return;
   const int64_t ifine = DIR == 0 ? i0 : (DIR == 1 ? i1 : i2);
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256)
 template <int K, typename T, int DIR>
 __global__ void __launch_bounds__(256)
     restrict_pass_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ in,
-                         T *__restrict__ out, int64_t e0, int64_t e1, int64_t e2, int64_t mf)
+                         T *__restrict__ out, int64_t e0, int64_t e1, int64_t e2, int64_t mf, int64_t z0)
 {
   pdl_prologue();
   __shared__ T Ps[2 * K + 1][K + 1];
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x;
   const int64_t i1 = static_cast<int64_t>(blockIdx.y) * 8 + threadIdx.y;
-  const int64_t i2 = blockIdx.z;
+  const int64_t i2 = z0 + blockIdx.z;  // global plane (slab callers shift their bases)
   if (i0 >= e0 || i1 >= e1)
     return;
   const int64_t icoarse = DIR == 0 ? i0 : (DIR == 1 ? i1 : i2);
@@ -167,7 +167,7 @@ struct Prol3Cfg
 template <int K, typename T, bool ACC>
 __global__ void __launch_bounds__(Prol3Cfg<K>::NT)
     prolong3d_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ xc, T *__restrict__ xf,
-                     int mc, int nc)
+                     int mc, int nc, int cz0, int f0, int f1)
 {
   pdl_prologue();
   using C = Prol3Cfg<K>;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(Prol3Cfg<K>::NT)
   const int tid = threadIdx.y * 32 + threadIdx.x;
   for (int e = tid; e < (2 * K + 1) * (K + 1); e += NT)
     (&Ps[0][0])[e] = (&P.P[0][0])[e];
-  const int cx0 = blockIdx.x * CX, cy0 = blockIdx.y * CY, cz = blockIdx.z;
+  const int cx0 = blockIdx.x * CX, cy0 = blockIdx.y * CY, cz = cz0 + blockIdx.z;
   const int64_t mc2 = static_cast<int64_t>(mc) * mc;
   // coarse lattice q = cK + t (1-based; 0 and mc+1 are the Dirichlet boundary)
   for (int e = tid; e < QZ * QY * QX; e += NT)
@@ -234,8 +234,10 @@ __global__ void __launch_bounds__(Prol3Cfg<K>::NT)
   for (int rz = 1; rz <= 2 * K; ++rz)
   {
     const int pz = 2 * cz * K + rz;
-    if (pz > mf)
+    if (pz > mf || pz - 1 >= f1)
       break;
+    if (pz - 1 < f0)  // fine planes [f0, f1) only (0-based)
+      continue;
     T s = T(0);
 #pragma unroll
     for (int t = 0; t <= K; ++t)
@@ -255,12 +257,12 @@ void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, in
   const int64_t mf = 2 * mc + 1;
   if constexpr (D == 2)
   {
-    pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf, mc, 1), dim3(32, 8), 0, s, P, xc, tA, mf, mc, 1, mc);
+    pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf, mc, 1), dim3(32, 8), 0, s, P, xc, tA, mf, mc, 1, mc, int64_t(0));
     check_launch("prolong_pass0");
     if (acc)
-      pdl_launch(prolong_pass_kernel<K, T, 1, true>, pass_grid(mf, mf, 1), dim3(32, 8), 0, s, P, tA, xf, mf, mf, 1, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 1, true>, pass_grid(mf, mf, 1), dim3(32, 8), 0, s, P, tA, xf, mf, mf, 1, mc, int64_t(0));
     else
-      pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf, mf, 1), dim3(32, 8), 0, s, P, tA, xf, mf, mf, 1, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf, mf, 1), dim3(32, 8), 0, s, P, tA, xf, mf, mf, 1, mc, int64_t(0));
     check_launch("prolong_pass1");
   }
   else if (use_fused_transfer())
@@ -269,21 +271,23 @@ void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, in
     const int nc = static_cast<int>((mc + 1) / K);  // coarse cells per direction
     const dim3 grid((nc + C::CX - 1) / C::CX, (nc + C::CY - 1) / C::CY, nc);
     if (acc)
-      pdl_launch(prolong3d_kernel<K, T, true>, grid, dim3(32, C::FY), 0, s, P, xc, xf, static_cast<int>(mc), nc);
+      pdl_launch(prolong3d_kernel<K, T, true>, grid, dim3(32, C::FY), 0, s, P, xc, xf, static_cast<int>(mc), nc, 0,
+                 0, static_cast<int>(mf));
     else
-      pdl_launch(prolong3d_kernel<K, T, false>, grid, dim3(32, C::FY), 0, s, P, xc, xf, static_cast<int>(mc), nc);
+      pdl_launch(prolong3d_kernel<K, T, false>, grid, dim3(32, C::FY), 0, s, P, xc, xf, static_cast<int>(mc), nc, 0,
+                 0, static_cast<int>(mf));
     check_launch("prolong3d_kernel");
   }
   else
   {
-    pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf, mc, mc), dim3(32, 8), 0, s, P, xc, tA, mf, mc, mc, mc);
+    pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf, mc, mc), dim3(32, 8), 0, s, P, xc, tA, mf, mc, mc, mc, int64_t(0));
     check_launch("prolong_pass0");
-    pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf, mf, mc), dim3(32, 8), 0, s, P, tA, tB, mf, mf, mc, mc);
+    pdl_launch(prolong_pass_kernel<K, T, 1, false>, pass_grid(mf, mf, mc), dim3(32, 8), 0, s, P, tA, tB, mf, mf, mc, mc, int64_t(0));
     check_launch("prolong_pass1");
     if (acc)
-      pdl_launch(prolong_pass_kernel<K, T, 2, true>, pass_grid(mf, mf, mf), dim3(32, 8), 0, s, P, tB, xf, mf, mf, mf, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 2, true>, pass_grid(mf, mf, mf), dim3(32, 8), 0, s, P, tB, xf, mf, mf, mf, mc, int64_t(0));
     else
-      pdl_launch(prolong_pass_kernel<K, T, 2, false>, pass_grid(mf, mf, mf), dim3(32, 8), 0, s, P, tB, xf, mf, mf, mf, mc);
+      pdl_launch(prolong_pass_kernel<K, T, 2, false>, pass_grid(mf, mf, mf), dim3(32, 8), 0, s, P, tB, xf, mf, mf, mf, mc, int64_t(0));
     check_launch("prolong_pass2");
   }
 }
@@ -295,20 +299,78 @@ void launch_restrict(const ProlMats<T, K> &P, const T *rf, T *rc, int64_t mc, T 
   const int64_t mf = 2 * mc + 1;
   if constexpr (D == 2)
   {
-    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, 1), dim3(32, 8), 0, s, P, rf, tA, mc, mf, 1, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, 1), dim3(32, 8), 0, s, P, rf, tA, mc, mf, 1, mf, int64_t(0));
     check_launch("restrict_pass0");
-    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, 1), dim3(32, 8), 0, s, P, tA, rc, mc, mc, 1, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, 1), dim3(32, 8), 0, s, P, tA, rc, mc, mc, 1, mf, int64_t(0));
     check_launch("restrict_pass1");
   }
   else
   {
-    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, mf), dim3(32, 8), 0, s, P, rf, tA, mc, mf, mf, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, mf), dim3(32, 8), 0, s, P, rf, tA, mc, mf, mf, mf, int64_t(0));
     check_launch("restrict_pass0");
-    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, mf), dim3(32, 8), 0, s, P, tA, tB, mc, mc, mf, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, mf), dim3(32, 8), 0, s, P, tA, tB, mc, mc, mf, mf, int64_t(0));
     check_launch("restrict_pass1");
-    pdl_launch(restrict_pass_kernel<K, T, 2>, pass_grid(mc, mc, mc), dim3(32, 8), 0, s, P, tB, rc, mc, mc, mc, mf);
+    pdl_launch(restrict_pass_kernel<K, T, 2>, pass_grid(mc, mc, mc), dim3(32, 8), 0, s, P, tB, rc, mc, mc, mc, mf, int64_t(0));
     check_launch("restrict_pass2");
   }
+}
+
+// ---------------------------------------------------------------------------
+// Slab versions (3D; the slab domain decomposition's V-cycle, dd.py). All
+// pointers are GLOBAL-plane bases (the caller shifts its local array by its
+// first plane); only the planes the requested outputs depend on are touched.
+// ---------------------------------------------------------------------------
+
+// fine planes [f0, f1) (0-based) (+)= P x_c
+template <int K, typename T>
+void launch_prolongate_slab(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, int64_t mc, int64_t f0,
+                            int64_t f1, cudaStream_t s)
+{
+  using C = Prol3Cfg<K>;
+  if (f1 <= f0)
+    return;
+  const int nc = static_cast<int>((mc + 1) / K);
+  const int cz0 = static_cast<int>(f0 / (2 * K)), cz1 = static_cast<int>((f1 - 1) / (2 * K));
+  const dim3 grid((nc + C::CX - 1) / C::CX, (nc + C::CY - 1) / C::CY, cz1 - cz0 + 1);
+  if (acc)
+    pdl_launch(prolong3d_kernel<K, T, true>, grid, dim3(32, C::FY), 0, s, P, xc, xf, static_cast<int>(mc), nc, cz0,
+               static_cast<int>(f0), static_cast<int>(f1));
+  else
+    pdl_launch(prolong3d_kernel<K, T, false>, grid, dim3(32, C::FY), 0, s, P, xc, xf, static_cast<int>(mc), nc, cz0,
+               static_cast<int>(f0), static_cast<int>(f1));
+  check_launch("prolong3d_kernel(slab)");
+}
+
+// fine planes the coarse planes [q0, q1) depend on: [pz0, pz1) (0-based)
+inline void restrict_slab_fine_range(int K, int64_t mc, int64_t q0, int64_t q1, int64_t &pz0, int64_t &pz1)
+{
+  const int64_t mf = 2 * mc + 1;
+  const int64_t cmin = std::max<int64_t>(0, (q0 + 1 - K + K - 1) / K);  // ceil((Q0 - K) / K), Q0 = q0 + 1
+  const int64_t cmax = q1 / K;                                           // floor(Q1 / K), Q1 = q1
+  pz0 = 2 * cmin * K;
+  pz1 = std::min<int64_t>(2 * cmax * K + 2 * K, mf);
+}
+
+// coarse planes [q0, q1) = R r_f; tA, tB: local scratch of mc*mf and mc*mc
+// per fine plane of [pz0, pz1) (global-plane bases, as the vectors)
+template <int K, typename T>
+void launch_restrict_slab(const ProlMats<T, K> &P, const T *rf, T *rc, int64_t mc, int64_t q0, int64_t q1, T *tA,
+                          T *tB, cudaStream_t s)
+{
+  if (q1 <= q0)
+    return;
+  const int64_t mf = 2 * mc + 1;
+  int64_t pz0, pz1;
+  restrict_slab_fine_range(K, mc, q0, q1, pz0, pz1);
+  pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, pz1 - pz0), dim3(32, 8), 0, s, P, rf, tA, mc, mf, mf,
+             mf, pz0);
+  check_launch("restrict_pass0(slab)");
+  pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, pz1 - pz0), dim3(32, 8), 0, s, P, tA, tB, mc, mc, mf,
+             mf, pz0);
+  check_launch("restrict_pass1(slab)");
+  pdl_launch(restrict_pass_kernel<K, T, 2>, pass_grid(mc, mc, q1 - q0), dim3(32, 8), 0, s, P, tB, rc, mc, mc, mc,
+             mf, q0);
+  check_launch("restrict_pass2(slab)");
 }
 
 }  // namespace pmgb

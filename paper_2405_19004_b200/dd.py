@@ -28,6 +28,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 
 @dataclass(frozen=True)
 class SlabPlan:
@@ -249,3 +251,234 @@ class StagedComm:
                     x[l0 * ps:(l0 + n) * ps].copy_(buf)
 
         return H()
+
+
+# ---------------------------------------------------------------------------
+# The V-cycle on z-slabs (SURVEY.md §8e "rest of the V-cycle").
+#
+# Levels whose slabs are thick enough (every rank owns >= 2 H dof planes,
+# H = 4k + 4) are decomposed; below that the level is agglomerated: its
+# right-hand side is all-gathered and every rank runs the remaining V-cycle
+# redundantly on the whole (small) level, so no broadcast is needed. On a
+# decomposed level each rank keeps its vectors on the planes E = [lo - H,
+# hi + H] (clipped), the smoother's slab [lo, hi] plus halo:
+#
+#   pre-smooth (SlabSmoother, per-colour one-directional plane messages)
+#   halo(x)                      neighbours' owned planes -> E
+#   r = b - A x on owned planes  (residual_slab), halo(r)
+#   b_c = R r on coarse owned planes (restrict_slab), halo(b_c), x_c = 0
+#   recurse; halo(x_c)
+#   x += P x_c on [lo, hi]       (prolongate_slab; the halo planes of [lo, hi]
+#                                 get the same update as their owner's copy)
+#   post-smooth
+#
+# Every value is computed by the same per-output arithmetic as the
+# single-domain V-cycle (multigrid.cpp:313-348), so P ranks reproduce it
+# bitwise. The operations are supplied by a backend (GPU C-ABI slab entry
+# points, or the numpy oracle in the CPU tests); messages by a communicator
+# factory (torch.distributed NCCL / gloo).
+# ---------------------------------------------------------------------------
+
+
+def halo_width(k: int) -> int:
+    return 4 * k + 4
+
+
+@dataclass(frozen=True)
+class LevelSlab:
+    level: int
+    plan: SlabPlan
+    e0: int  # first global dof plane held (extended slab E)
+    e1: int  # last (inclusive)
+
+    @property
+    def n(self) -> int:
+        return self.e1 - self.e0 + 1
+
+
+def level_slab(world: int, rank: int, k: int, level: int) -> LevelSlab:
+    p = make_plan(world, rank, k, level)
+    H = halo_width(k)
+    return LevelSlab(level, p, max(0, p.lo - H), min(p.mz - 1, p.hi + H))
+
+
+def decomposed_levels(world: int, k: int, finest: int) -> list:
+    """Levels (finest first) on which every rank owns >= 2 H planes."""
+    out = []
+    for lev in range(finest, 1, -1):
+        n = 1 << lev
+        if n - 1 < world:
+            break
+        plans = [make_plan(world, r, k, lev) for r in range(world)]
+        if min(p.own_hi - p.own_lo + 1 for p in plans) < 2 * halo_width(k):
+            break
+        out.append(lev)
+    return out
+
+
+def _exchange_specs(world: int, rank: int, slabs_by_rank):
+    """(sends, recvs) of local-plane ranges that bring every plane of my E
+    outside my owned range from its owner, and give my neighbours theirs."""
+    me = slabs_by_rank[rank]
+    sends, recvs = [], []
+    for q in (rank - 1, rank + 1):
+        if not 0 <= q < world:
+            continue
+        nb = slabs_by_rank[q]
+        # planes of my E owned by q
+        lo = max(me.e0, nb.plan.own_lo)
+        hi = min(me.e1, nb.plan.own_hi)
+        if lo <= hi:
+            recvs.append((q, lo - me.e0, hi - lo + 1))
+        # planes of q's E owned by me
+        lo = max(nb.e0, me.plan.own_lo)
+        hi = min(nb.e1, me.plan.own_hi)
+        if lo <= hi:
+            sends.append((q, lo - me.e0, hi - lo + 1))
+    return sends, recvs
+
+
+class SlabVCycle:
+    """One V-cycle (pre = post = 1) of the slab-decomposed hierarchy.
+
+    ops: backend with
+      kernel(level, slab, x_view, b_view) -> colour kernel for SlabSmoother
+      residual(level, x, b, r, e0, p0, p1)
+      restrict(level_f, rf, e0_f, rc, e0_c, q0, q1)
+      prolongate(level_f, xc, e0_c, xf, e0_f, f0, f1)        (accumulating)
+      vcycle_full(level, b_full) -> x_full                    (agglomerated)
+      zeros(n), view(a, start, count), owned_slice(...)
+    comm(array, plane_size) -> object with post(sends, recvs).wait()
+    allgather(array) -> list of arrays from all ranks (rank order)
+    """
+
+    def __init__(self, world, rank, k, finest, ops, comm, allgather):
+        self.world, self.rank, self.k, self.finest = world, rank, k, finest
+        self.ops, self.comm, self.allgather = ops, comm, allgather
+        self.dd_levels = decomposed_levels(world, k, finest)
+        if not self.dd_levels or self.dd_levels[0] != finest:
+            raise ValueError("finest level too thin for the slab decomposition on this many ranks")
+        self.agg = self.dd_levels[-1] - 1  # first agglomerated level
+        self.slabs = {lev: [level_slab(world, r, k, lev) for r in range(world)] for lev in self.dd_levels}
+        self.ex = {lev: _exchange_specs(world, rank, self.slabs[lev]) for lev in self.dd_levels}
+        self.ps = {lev: ((1 << lev) * k - 1) ** 2 for lev in range(1, finest + 1)}
+        # work vectors per decomposed level (finest: x, b are the caller's)
+        self.r, self.bc, self.xc = {}, {}, {}
+        for lev in self.dd_levels:
+            n = self.slabs[lev][rank].n * self.ps[lev]
+            self.r[lev] = ops.zeros(n)
+            if lev - 1 in self.slabs:
+                nc = self.slabs[lev - 1][rank].n * self.ps[lev - 1]
+            else:
+                nc = self.ps[lev - 1] * ((1 << (lev - 1)) * k - 1)  # the whole agglomerated level
+            self.bc[lev] = ops.zeros(nc)
+            self.xc[lev] = ops.zeros(nc)
+
+    def slab(self, lev) -> LevelSlab:
+        return self.slabs[lev][self.rank]
+
+    def halo(self, lev, a):
+        sends, recvs = self.ex[lev]
+        if sends or recvs:
+            self.comm(a, self.ps[lev]).post(sends, recvs).wait()
+
+    def _smooth(self, lev, x, b):
+        s, ps = self.slab(lev), self.ps[lev]
+        off = (s.plan.lo - s.e0) * ps
+        cnt = s.plan.nplanes * ps
+        xv, bv = self.ops.view(x, off, cnt), self.ops.view(b, off, cnt)
+        SlabSmoother(s.plan, self.ops.kernel(lev, s.plan, xv, bv), self.comm(xv, ps)).smooth()
+
+    def _gather_full(self, lev, a):
+        """Owned planes of every rank -> the whole level vector."""
+        s, ps = self.slab(lev), self.ps[lev]
+        own = self.ops.view(a, (s.plan.own_lo - s.e0) * ps, (s.plan.own_hi - s.plan.own_lo + 1) * ps)
+        return self.ops.cat(self.allgather(own))
+
+    def vcycle(self, lev, x, b):
+        s, ps = self.slab(lev), self.ps[lev]
+        p = s.plan
+        self._smooth(lev, x, b)
+        self.halo(lev, x)
+        self.ops.residual(lev, x, b, self.r[lev], s.e0, p.own_lo, p.own_hi + 1)
+        self.halo(lev, self.r[lev])
+        bc, xc = self.bc[lev], self.xc[lev]
+        if lev - 1 in self.slabs:
+            sc = self.slab(lev - 1)
+            self.ops.restrict(lev, self.r[lev], s.e0, bc, sc.e0, sc.plan.own_lo, sc.plan.own_hi + 1)
+            self.halo(lev - 1, bc)
+            self.ops.fill(xc, 0.0)
+            self.vcycle(lev - 1, xc, bc)
+            self.halo(lev - 1, xc)
+            e0c = sc.e0
+        else:
+            # agglomerated coarse level: this rank's share of R r, gathered,
+            # then the rest of the V-cycle on the whole level (redundantly)
+            mc = (1 << (lev - 1)) * self.k - 1
+            q0, q1 = self._coarse_share(lev)
+            self.ops.fill(bc, 0.0)
+            self.ops.restrict(lev, self.r[lev], s.e0, bc, 0, q0, q1)
+            part = self.ops.view(bc, q0 * self.ps[lev - 1], (q1 - q0) * self.ps[lev - 1])
+            full_b = self.ops.cat(self.allgather(part))
+            xfull = self.ops.vcycle_full(lev - 1, full_b)
+            self.ops.copy(xc, xfull)
+            e0c = 0
+            del mc
+        self.ops.prolongate(lev, xc, e0c, x, s.e0, p.lo, p.hi + 1)
+        self._smooth(lev, x, b)
+
+    def _coarse_share(self, lev):
+        """Coarse planes this rank restricts at the agglomeration boundary: a
+        contiguous partition of [0, mc) proportional to the fine ownership."""
+        mc = (1 << (lev - 1)) * self.k - 1
+        p = self.slab(lev).plan
+        mf = p.mz
+        q0 = 0 if self.rank == 0 else (p.own_lo * mc) // mf
+        q1 = mc if self.rank == self.world - 1 else ((p.own_hi + 1) * mc) // mf
+        return q0, q1
+
+
+class GpuSlabOps:
+    """SlabVCycle backend on the device: the C-ABI slab entry points of a
+    MultigridContext (pmg.py) on CUDA tensors."""
+
+    def __init__(self, mg, variant: str = "fused"):
+        import torch
+
+        from . import pmg as _pmg
+
+        self.pmg, self.torch, self.mg, self.variant = _pmg, torch, mg, variant
+        self.lv = {lc.level.level: lc for lc in mg.levels}
+        self.dtype = torch.float64 if mg.levels[-1].dtype == np.float64 else torch.float32
+
+    def zeros(self, n):
+        return self.torch.zeros(n, dtype=self.dtype, device=f"cuda:{self.mg.device}")
+
+    def view(self, a, off, cnt):
+        return a[off:off + cnt]
+
+    def fill(self, a, v):
+        a.fill_(v)
+
+    def cat(self, parts):
+        return self.torch.cat(parts)
+
+    def copy(self, dst, src):
+        dst.copy_(src)
+
+    def kernel(self, lev, plan, xv, bv):
+        return gpu_kernel(self.lv[lev], plan, xv, bv, self.variant)
+
+    def residual(self, lev, x, b, r, e0, p0, p1):
+        self.pmg.compute_residual_slab(self.lv[lev], x, b, r, e0, p0, p1)
+
+    def restrict(self, lev, rf, e0f, rc, e0c, q0, q1):
+        self.pmg.restrict_slab(self.lv[lev - 1], self.lv[lev], rf, e0f, rc, e0c, q0, q1)
+
+    def prolongate(self, lev, xc, e0c, xf, e0f, f0, f1):
+        self.pmg.prolongate_slab(self.lv[lev - 1], self.lv[lev], xc, e0c, xf, e0f, f0, f1, True)
+
+    def vcycle_full(self, lev, b):
+        x = self.zeros(b.numel())
+        self.pmg.v_cycle(self.mg, lev - 1, x, b)
+        return x

@@ -37,6 +37,7 @@ __all__ = [
     "apply_laplacian", "compute_residual", "prolongate", "restrict_vector", "v_cycle",
     "full_multigrid", "FmgStats", "vector_norm", "compute_rhs", "l2_error", "gmres", "SolveStats",
     "DivergenceError", "set_smoother_impl", "get_smoother_impl", "compute_rhs_device",
+    "compute_residual_slab", "restrict_slab", "prolongate_slab",
 ]
 
 _SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2, "sweep": 3}
@@ -349,6 +350,51 @@ def restrict_vector(coarse: LevelContext, fine: LevelContext, r_fine, r_coarse) 
               "restrict_vector")
     else:
         check(lib.pmg_restrict_vector_host(coarse.handle, fine.handle, rf.ptr, rc.ptr), "restrict_vector")
+
+
+# ---------------------------------------------------------------------------
+# slab operations of the z-slab domain decomposition (dd.py). Arrays are CUDA
+# tensors holding the global dof planes [zoff, zoff + numel / m^2).
+# ---------------------------------------------------------------------------
+
+
+def _slab(ctx: LevelContext, a, name: str, writable: bool):
+    m = ctx.level.dofs_per_dim
+    if not (_is_torch(a) and a.is_cuda):
+        raise TypeError(f"{name}: slab operations take CUDA tensors")
+    if a.numel() % (m * m):
+        raise ValueError(f"{name}: not a whole number of planes")
+    return _Arr(a, a.numel(), ctx._code, name, writable), a.numel() // (m * m)
+
+
+def compute_residual_slab(ctx: LevelContext, x, b, r, zoff: int, p0: int, p1: int) -> None:
+    """r = b - A x on global planes [p0, p1) (multigrid.cpp:268-276); x, b, r
+    hold the same planes [zoff, zoff + n)."""
+    ax, n = _slab(ctx, x, "x", False)
+    ab, nb = _slab(ctx, b, "b", False)
+    ar, nr = _slab(ctx, r, "r", True)
+    if not n == nb == nr:
+        raise ValueError("compute_residual_slab: x, b, r must hold the same planes")
+    check(_lib.load().pmg_compute_residual_slab(ctx.handle, ax.ptr, ab.ptr, ar.ptr, zoff, n, p0, p1, _stream([x])),
+          "compute_residual_slab")
+
+
+def restrict_slab(coarse: LevelContext, fine: LevelContext, rf, zoff_f: int, rc, zoff_c: int, q0: int,
+                  q1: int) -> None:
+    """Coarse planes [q0, q1) of R r_f (multigrid.cpp:162-248)."""
+    af, nf = _slab(fine, rf, "rf", False)
+    ac, nc = _slab(coarse, rc, "rc", True)
+    check(_lib.load().pmg_restrict_slab(coarse.handle, fine.handle, af.ptr, zoff_f, nf, ac.ptr, zoff_c, nc, q0, q1,
+                                        _stream([rf])), "restrict_slab")
+
+
+def prolongate_slab(coarse: LevelContext, fine: LevelContext, xc, zoff_c: int, xf, zoff_f: int, f0: int, f1: int,
+                    accumulate: bool = True) -> None:
+    """Fine planes [f0, f1) (+)= P x_c (multigrid.cpp:71-160)."""
+    ac, nc = _slab(coarse, xc, "xc", False)
+    af, nf = _slab(fine, xf, "xf", True)
+    check(_lib.load().pmg_prolongate_slab(coarse.handle, fine.handle, ac.ptr, zoff_c, nc, af.ptr, zoff_f, nf, f0, f1,
+                                          1 if accumulate else 0, _stream([xf])), "prolongate_slab")
 
 
 def vector_norm(v, device: int = 0) -> float:

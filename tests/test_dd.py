@@ -133,3 +133,116 @@ def test_gloo_two_ranks(tmp_path, stack):
     mp.spawn(_gloo_worker, args=(2, _free_port(), 2, 3, stack, out), nprocs=2, join=True)
     err, scale = np.load(out)
     assert err <= 1e-13 * scale
+
+
+# ---------------------------------------------------------------------------
+# The slab-decomposed V-cycle (dd.SlabVCycle) with the numpy oracle as the
+# backend: P ranks over gloo == the oracle's single-domain V-cycle.
+# ---------------------------------------------------------------------------
+
+
+class OracleSlabOps:
+    """dd.SlabVCycle backend on the CPU: every slab operation embeds the slab
+    into a zero global vector, applies the oracle's full-domain operation and
+    keeps the requested planes (which only depend on planes the slab holds)."""
+
+    def __init__(self, octx):
+        self.o = octx
+        self.lc = {lc.level.level: lc for lc in octx.levels}
+
+    def ps(self, lev):
+        return self.lc[lev].level.dofs_per_dim ** 2
+
+    def embed(self, lev, a, e0):
+        full = np.zeros(self.lc[lev].level.total_dofs)
+        full[e0 * self.ps(lev):e0 * self.ps(lev) + a.size] = a
+        return full
+
+    def zeros(self, n):
+        return np.zeros(n)
+
+    def view(self, a, off, cnt):
+        return a[off:off + cnt]
+
+    def fill(self, a, v):
+        a[:] = v
+
+    def cat(self, parts):
+        return np.concatenate([np.asarray(p) for p in parts])
+
+    def copy(self, dst, src):
+        dst[:] = src
+
+    def kernel(self, lev, plan, xv, bv):
+        lc = self.lc[lev]
+        return lambda c, vlo, vhi: O.smooth_colour_slab(lc, xv, bv, c, plan.lo, plan.nz, vlo, vhi)
+
+    def residual(self, lev, x, b, r, e0, p0, p1):
+        ps = self.ps(lev)
+        rf = O.compute_residual(self.lc[lev], self.embed(lev, x, e0), self.embed(lev, b, e0))
+        r[(p0 - e0) * ps:(p1 - e0) * ps] = rf[p0 * ps:p1 * ps]
+
+    def restrict(self, lev, rf, e0f, rc, e0c, q0, q1):
+        psc = self.ps(lev - 1)
+        full = O.restrict_vector(self.lc[lev - 1], self.lc[lev], self.embed(lev, rf, e0f))
+        rc[(q0 - e0c) * psc:(q1 - e0c) * psc] = full[q0 * psc:q1 * psc]
+
+    def prolongate(self, lev, xc, e0c, xf, e0f, f0, f1):
+        ps = self.ps(lev)
+        full = O.prolongate(self.lc[lev - 1], self.lc[lev], self.embed(lev - 1, xc, e0c))
+        xf[(f0 - e0f) * ps:(f1 - e0f) * ps] += full[f0 * ps:f1 * ps]
+
+    def vcycle_full(self, lev, b):
+        return O.v_cycle(self.o, lev - 1, np.zeros_like(b), b)
+
+
+def _gloo_vcycle_worker(rank, world, port, k, level, out_path):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        octx = O.MultigridContext(3, k, level)
+        n = octx.levels[-1].level.total_dofs
+        rng = np.random.default_rng(31)
+        x0, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+
+        def comm(a, ps):
+            return dd.TorchDistComm(torch.from_numpy(a), ps)
+
+        def allgather(part):
+            t = torch.from_numpy(np.ascontiguousarray(part))
+            sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(sizes, torch.tensor([t.numel()]))
+            mx = int(max(s.item() for s in sizes))
+            padded = torch.zeros(mx, dtype=t.dtype)
+            padded[: t.numel()] = t
+            parts = [torch.zeros(mx, dtype=t.dtype) for _ in sizes]
+            dist.all_gather(parts, padded)
+            return [p[: int(s.item())].numpy() for p, s in zip(parts, sizes)]
+
+        vc = dd.SlabVCycle(world, rank, k, level, OracleSlabOps(octx), comm, allgather)
+        s = vc.slab(level)
+        ps = s.plan.plane_size
+        x = x0[s.e0 * ps:(s.e1 + 1) * ps].copy()
+        bl = b[s.e0 * ps:(s.e1 + 1) * ps].copy()
+        vc.vcycle(level, x, bl)
+        own = x[(s.plan.own_lo - s.e0) * ps:(s.plan.own_hi - s.e0 + 1) * ps]
+        got = np.concatenate(allgather(own))
+        if rank == 0:
+            want = O.v_cycle(octx, level - 1, x0.copy(), b)
+            np.save(out_path, np.array([np.abs(got - want).max(), np.abs(want).max(), vc.agg]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k,level", [(2, 1, 6), (2, 2, 5), (3, 1, 6)])
+def test_gloo_slab_vcycle(tmp_path, world, k, level):
+    """The slab-decomposed V-cycle over gloo == the single-domain V-cycle."""
+    out = str(tmp_path / "err.npy")
+    mp.spawn(_gloo_vcycle_worker, args=(world, _free_port(), k, level, out), nprocs=world, join=True)
+    err, scale, agg = np.load(out)
+    assert agg >= 1
+    assert err <= 1e-13 * scale, (err, scale)
