@@ -8,6 +8,7 @@
 #include "smoother_plane.cuh"
 #include "smoother_point.cuh"
 #include "smoother_pp.cuh"
+#include "smoother_patch2d.cuh"
 #include "transfer_impl.cuh"
 
 #define PMG_CAT2(a, b) a##b
@@ -41,6 +42,18 @@ void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, 
         launch_vp_point<D, T, MODE_FUSED>(st, a, s);
       else
         launch_vp_point<D, T, MODE_BOUNDARY>(st, a, s);
+      return;
+    }
+  }
+  if constexpr (D == 2 && PMG_K == 2)
+  {
+    // 2D degree 2: one thread per patch, all in registers (smoother_patch2d.cuh)
+    if (impl != SMOOTHER_IMPL_LINE && (mode == MODE_FUSED || mode == MODE_BOUNDARY))
+    {
+      if (mode == MODE_FUSED)
+        launch_vp_patch2d<PMG_K, T, MODE_FUSED>(PM, a, s);
+      else
+        launch_vp_patch2d<PMG_K, T, MODE_BOUNDARY>(PM, a, s);
       return;
     }
   }
