@@ -21,6 +21,9 @@ namespace
 
 // 3D fused / boundary sweeps of degree <= PMG_PLANE_KMAX use the plane-streaming
 // kernel (smoother_plane.cuh) unless pmg_set_smoother_impl selects the line one
+#ifndef PMG_PATCH2D_KMAX
+#define PMG_PATCH2D_KMAX 3
+#endif
 #ifndef PMG_PLANE_KMAX
 #define PMG_PLANE_KMAX 2
 #endif
@@ -45,9 +48,9 @@ void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, 
       return;
     }
   }
-  if constexpr (D == 2 && PMG_K == 2)
+  if constexpr (D == 2 && PMG_K >= 2 && PMG_K <= PMG_PATCH2D_KMAX)
   {
-    // 2D degree 2: one thread per patch, all in registers (smoother_patch2d.cuh)
+    // 2D degree 2..: one thread per patch, all in registers (smoother_patch2d.cuh)
     if (impl != SMOOTHER_IMPL_LINE && (mode == MODE_FUSED || mode == MODE_BOUNDARY))
     {
       if (mode == MODE_FUSED)

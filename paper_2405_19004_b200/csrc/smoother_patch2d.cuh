@@ -1,7 +1,8 @@
 // 2D vertex-patch smoother with one thread per patch, for low degree (sm_100a).
 //
 // In 2D a Q_k patch (closure (2k+1)^2, interior (2k-1)^2) is small enough for
-// one thread to hold it in registers for k <= 2, so the per-patch body of the
+// one thread to hold it in registers for k <= 3 (closure rows are streamed,
+// the dir-1 contraction accumulated row pair by row pair), so the per-patch body of the
 // reference's fused / boundary smoother (smoother.cpp:109-148) runs without
 // shared memory or barriers: closure rows read through L1 (no patch of a
 // colour reads a node another patch of the colour writes, so the read-only
@@ -15,12 +16,11 @@
 namespace pmgb
 {
 
+// k <= 2: the whole closure's dir-0 contractions are kept in registers
 template <int K, typename T, int MODE>
-__global__ void __launch_bounds__(128) vp_patch2d_kernel(const __grid_constant__ PatchMatsEO<T, K> P,
-                                                         const __grid_constant__ ColorArgs<T> a)
+__device__ __forceinline__ void patch2d_regs(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a)
 {
   constexpr int NC = 2 * K + 1, NI = 2 * K - 1;
-  pdl_prologue();
   const int j0 = blockIdx.x * 32 + threadIdx.x;
   const int j1 = blockIdx.y * 4 + threadIdx.y;
   if (j0 >= a.np[0] || j1 >= a.np[1])
@@ -109,6 +109,144 @@ __global__ void __launch_bounds__(128) vp_patch2d_kernel(const __grid_constant__
         xp[i1 * m] = xold[i1][i0] + out[i1];
     }
   }
+}
+
+// k >= 3: closure rows streamed, dir 1 accumulated row pair by row pair
+template <int K, typename T, int MODE>
+__device__ __forceinline__ void patch2d_stream(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a)
+{
+  constexpr int NC = 2 * K + 1, NI = 2 * K - 1;
+  constexpr int HO = K > 1 ? K - 1 : 1;
+  const int j0 = blockIdx.x * 32 + threadIdx.x;
+  const int j1 = blockIdx.y * 4 + threadIdx.y;
+  if (j0 >= a.np[0] || j1 >= a.np[1])
+    return;
+  const int64_t m = a.m;
+  // closure origin g_a = k (v_a - 1) - 1, v_a = 2 j_a + vb_a (patches.cpp:71)
+  const int g0 = K * (2 * j0 + a.vb[0] - 1) - 1;
+  const int g1 = K * (2 * j1 + a.vb[1] - 1) - 1;
+  // closure row t1 -> dir 0 contractions zM = M0 u, zA = A0 u
+  auto row = [&](int t1, T (&zm)[NI], T (&za)[NI]) {
+    const int y = g1 + t1;
+    const bool oky = static_cast<unsigned>(y) < static_cast<unsigned>(m);
+    const T *rp = a.x + static_cast<int64_t>(y) * m + g0;
+    T u[NC], ue[K + 1], uo[K];
+#pragma unroll
+    for (int t0 = 0; t0 < NC; ++t0)
+    {
+      const bool ok = oky && static_cast<unsigned>(g0 + t0) < static_cast<unsigned>(m);
+      T v = ok ? __ldg(rp + t0) : T(0);
+      if constexpr (MODE == MODE_BOUNDARY)  // never reads x^I (smoother.cpp:128-148)
+        v = (t0 >= 1 && t0 <= NC - 2 && t1 >= 1 && t1 <= NC - 2) ? T(0) : v;
+      u[t0] = v;
+    }
+    eo_split<NC>(u, ue, uo);
+    eo_rows<K>(P.Me, P.Mo, ue, uo, zm);
+    eo_rows<K>(P.Ae, P.Ao, ue, uo, za);
+  };
+  // dir 1, accumulated row pair by row pair (even-odd in dir 1):
+  // acc = A1 zM + M1 zA, even part E[h][i0], odd part O[h][i0]
+  T E[K][NI], O[HO][NI];
+#pragma unroll
+  for (int jj = 0; jj <= K; ++jj)
+  {
+    T zma[NI], zaa[NI];
+    row(jj, zma, zaa);
+    if (jj < K)
+    {
+      T zmb[NI], zab[NI];
+      row(NC - 1 - jj, zmb, zab);
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+      {
+        const T zme = zma[i] + zmb[i], zmo = zma[i] - zmb[i];
+        const T zae = zaa[i] + zab[i], zao = zaa[i] - zab[i];
+#pragma unroll
+        for (int h = 0; h < K; ++h)
+          E[h][i] = jj == 0 ? fma(P.Ae[h][jj], zme, P.Me[h][jj] * zae)
+                            : fma(P.Ae[h][jj], zme, fma(P.Me[h][jj], zae, E[h][i]));
+#pragma unroll
+        for (int h = 0; h < K - 1; ++h)
+          O[h][i] = jj == 0 ? fma(P.Ao[h][jj], zmo, P.Mo[h][jj] * zao)
+                            : fma(P.Ao[h][jj], zmo, fma(P.Mo[h][jj], zao, O[h][i]));
+      }
+    }
+    else
+    {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+#pragma unroll
+        for (int h = 0; h < K; ++h)
+          E[h][i] = fma(P.Ae[h][K], zma[i], fma(P.Me[h][K], zaa[i], E[h][i]));
+    }
+  }
+  // r = b - acc; S^T along dir 1 (per column i0)
+  T y[NI][NI];  // [c1][i0]
+  const T *bb = a.b + static_cast<int64_t>(g1 + 1) * m + (g0 + 1);
+#pragma unroll
+  for (int i0 = 0; i0 < NI; ++i0)
+  {
+    T r[NI], yh[NI];
+#pragma unroll
+    for (int h = 0; h < K; ++h)
+    {
+      if (h < K - 1)
+      {
+        r[h] = __ldg(bb + h * m + i0) - (E[h][i0] + O[h][i0]);
+        r[NI - 1 - h] = __ldg(bb + (NI - 1 - h) * m + i0) - (E[h][i0] - O[h][i0]);
+      }
+      else
+        r[h] = __ldg(bb + h * m + i0) - E[h][i0];
+    }
+    eo_st<K>(P.Se, P.So, r, yh);
+#pragma unroll
+    for (int c1 = 0; c1 < NI; ++c1)
+      y[c1][i0] = yh[c1];
+  }
+  // dir 0: S^T, scale by 1/(lambda sums), S (per eigen row c1)
+#pragma unroll
+  for (int c1 = 0; c1 < NI; ++c1)
+  {
+    T yh[NI], v[NI];
+    eo_st<K>(P.Se, P.So, y[c1], yh);
+#pragma unroll
+    for (int c0 = 0; c0 < NI; ++c0)
+      yh[c0] *= __ldg(a.inv + c0 + NI * c1);
+    eo_s<K>(P.Se, P.So, yh, v);
+#pragma unroll
+    for (int i0 = 0; i0 < NI; ++i0)
+      y[c1][i0] = v[i0];
+  }
+  // S along dir 1, x^I update (x^I_old re-read: only this thread writes it)
+  T *xp = a.x + static_cast<int64_t>(g1 + 1) * m + (g0 + 1);
+#pragma unroll
+  for (int i0 = 0; i0 < NI; ++i0)
+  {
+    T col[NI], out[NI];
+#pragma unroll
+    for (int c1 = 0; c1 < NI; ++c1)
+      col[c1] = y[c1][i0];
+    eo_s<K>(P.Se, P.So, col, out);
+#pragma unroll
+    for (int i1 = 0; i1 < NI; ++i1)
+    {
+      if constexpr (MODE == MODE_BOUNDARY)
+        xp[i1 * m + i0] = out[i1];
+      else
+        xp[i1 * m + i0] = __ldg(xp + i1 * m + i0) + out[i1];
+    }
+  }
+}
+
+template <int K, typename T, int MODE>
+__global__ void __launch_bounds__(128) vp_patch2d_kernel(const __grid_constant__ PatchMatsEO<T, K> P,
+                                                         const __grid_constant__ ColorArgs<T> a)
+{
+  pdl_prologue();
+  if constexpr (K <= 2)
+    patch2d_regs<K, T, MODE>(P, a);
+  else
+    patch2d_stream<K, T, MODE>(P, a);
 }
 
 template <int K, typename T, int MODE>
