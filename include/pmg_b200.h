@@ -210,7 +210,7 @@ int64_t pmg_launch_count(void);
  * default, 1 = line-per-thread kernel everywhere, 2 = plane-streaming kernel
  * where it exists (3D, degree <= 2, fused / boundary) with one launch per
  * colour (the default for degree 2), 3 = the same with all colours of a step
- * in one persistent launch. Results agree to rounding (2 and 3 bitwise);
+ * in one persistent launch, 4 = one thread per patch (3D degree 2). Results agree to rounding (2 and 3 bitwise);
  * used for A/B measurement. Returns PMG_ERR_INVALID otherwise. */
 int pmg_set_smoother_impl(int impl);
 int pmg_get_smoother_impl(void);

@@ -225,6 +225,10 @@ void level_init(pmg_level_s *l)
       v.insert(v.end(), w, w + 27);
       v.push_back(static_cast<T>(coef));
     }
+    // dense interior rows M_if, A_if and eigenvectors S (PatchMats<T,K>) last:
+    // the dir-2 contraction of the one-thread-per-patch 3D kernel
+    for (const Dense *dm : {&S.mass_if, &S.stiff_if, &S.S})
+      v.insert(v.end(), dm->a.begin(), dm->a.end());
     l->patch_mats.resize(v.size() * sizeof(T));
     std::memcpy(l->patch_mats.data(), v.data(), l->patch_mats.size());
   }
@@ -739,9 +743,9 @@ int64_t pmg_launch_count(void) { return g_launches.load(); }
 
 int pmg_set_smoother_impl(int impl)
 {
-  if (impl < SMOOTHER_IMPL_AUTO || impl > SMOOTHER_IMPL_SWEEP)
+  if (impl < SMOOTHER_IMPL_AUTO || impl > SMOOTHER_IMPL_PATCH)
   {
-    g_last_error = "pmg_set_smoother_impl: impl must be 0, 1, 2 or 3";
+    g_last_error = "pmg_set_smoother_impl: impl must be 0 .. 4";
     return PMG_ERR_INVALID;
   }
   g_smoother_impl.store(impl);

@@ -35,7 +35,8 @@ enum : int
   SMOOTHER_IMPL_AUTO = 0,
   SMOOTHER_IMPL_LINE = 1,
   SMOOTHER_IMPL_PLANE = 2,  // plane kernel, one launch per colour
-  SMOOTHER_IMPL_SWEEP = 3   // plane kernel, all colours in one persistent launch
+  SMOOTHER_IMPL_SWEEP = 3,  // plane kernel, all colours in one persistent launch
+  SMOOTHER_IMPL_PATCH = 4   // one thread per patch (3D k = 2, 2D k <= 3)
 };
 int smoother_impl_choice();
 void check_launch(const char *what);  // cudaGetLastError + count

@@ -261,3 +261,226 @@ void launch_vp_patch2d(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a, cudaSt
 }
 
 }  // namespace pmgb
+
+namespace pmgb
+{
+
+// ---------------------------------------------------------------------------
+// 3D, one thread per patch (k = 2): the closure is streamed plane by plane
+// (z-planes t2, rows t1 through L1), each plane contracted in dir 0 (per row)
+// and dir 1 (row pairs, even-odd) to wMM, wS (NI x NI), and dir 2 accumulated
+// densely into the NI^3 residual; then the 3D fast-diagonalisation solve in
+// registers and the x^I update. No shared memory, no barriers.
+// ---------------------------------------------------------------------------
+template <int K, typename T, int MODE>
+__global__ void __launch_bounds__(128, 3) vp_patch3d_kernel(const __grid_constant__ PatchMatsEO<T, K> P,
+                                                            const __grid_constant__ ColorArgs<T> a,
+                                                            const __grid_constant__ PatchMats<T, K> D)
+{
+  constexpr int NC = 2 * K + 1, NI = 2 * K - 1;
+  constexpr int HO = K > 1 ? K - 1 : 1;
+  pdl_prologue();
+  const int j0 = blockIdx.x * 32 + threadIdx.x;
+  const int j1 = blockIdx.y * 4 + threadIdx.y;
+  const int j2 = blockIdx.z;
+  if (j0 >= a.np[0] || j1 >= a.np[1])
+    return;
+  const int64_t m = a.m, m2 = m * m;
+  const int g0 = K * (2 * j0 + a.vb[0] - 1) - 1;
+  const int g1 = K * (2 * j1 + a.vb[1] - 1) - 1;
+  const int64_t g2 = static_cast<int64_t>(K) * (2 * j2 + a.vb[2] - 1) - 1;  // global plane
+  T acc[NI][NI][NI];  // [i2][i1][i0]: A-bar x on the interior
+#pragma unroll
+  for (int t2 = 0; t2 < NC; ++t2)
+  {
+    const bool okz = static_cast<uint64_t>(g2 + t2) < static_cast<uint64_t>(a.mz);
+    const T *pl = a.x + (g2 + t2 - a.zoff) * m2;
+    auto row = [&](int t1, T (&zm)[NI], T (&za)[NI]) {
+      const int y = g1 + t1;
+      const bool oky = okz && static_cast<unsigned>(y) < static_cast<unsigned>(m);
+      const T *rp = pl + static_cast<int64_t>(y) * m + g0;
+      T u[NC], ue[K + 1], uo[K];
+#pragma unroll
+      for (int t0 = 0; t0 < NC; ++t0)
+      {
+        const bool ok = oky && static_cast<unsigned>(g0 + t0) < static_cast<unsigned>(m);
+        T v = ok ? __ldg(rp + t0) : T(0);
+        if constexpr (MODE == MODE_BOUNDARY)  // never reads x^I (smoother.cpp:128-148)
+          v = (t0 >= 1 && t0 <= NC - 2 && t1 >= 1 && t1 <= NC - 2 && t2 >= 1 && t2 <= NC - 2) ? T(0) : v;
+        u[t0] = v;
+      }
+      eo_split<NC>(u, ue, uo);
+      eo_rows<K>(P.Me, P.Mo, ue, uo, zm);
+      eo_rows<K>(P.Ae, P.Ao, ue, uo, za);
+    };
+    // dir 1 (row pairs): wMM = M1 zM (Em/Om), wS = A1 zM + M1 zA (Es/Os)
+    T Em[K][NI], Om[HO][NI], Es[K][NI], Os[HO][NI];
+#pragma unroll
+    for (int jj = 0; jj <= K; ++jj)
+    {
+      T zma[NI], zaa[NI];
+      row(jj, zma, zaa);
+      if (jj < K)
+      {
+        T zmb[NI], zab[NI];
+        row(NC - 1 - jj, zmb, zab);
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+        {
+          const T zme = zma[i] + zmb[i], zmo = zma[i] - zmb[i];
+          const T zae = zaa[i] + zab[i], zao = zaa[i] - zab[i];
+#pragma unroll
+          for (int h = 0; h < K; ++h)
+          {
+            Em[h][i] = jj == 0 ? P.Me[h][jj] * zme : fma(P.Me[h][jj], zme, Em[h][i]);
+            Es[h][i] = jj == 0 ? fma(P.Ae[h][jj], zme, P.Me[h][jj] * zae)
+                               : fma(P.Ae[h][jj], zme, fma(P.Me[h][jj], zae, Es[h][i]));
+          }
+#pragma unroll
+          for (int h = 0; h < K - 1; ++h)
+          {
+            Om[h][i] = jj == 0 ? P.Mo[h][jj] * zmo : fma(P.Mo[h][jj], zmo, Om[h][i]);
+            Os[h][i] = jj == 0 ? fma(P.Ao[h][jj], zmo, P.Mo[h][jj] * zao)
+                               : fma(P.Ao[h][jj], zmo, fma(P.Mo[h][jj], zao, Os[h][i]));
+          }
+        }
+      }
+      else
+      {
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+#pragma unroll
+          for (int h = 0; h < K; ++h)
+          {
+            Em[h][i] = fma(P.Me[h][K], zma[i], Em[h][i]);
+            Es[h][i] = fma(P.Ae[h][K], zma[i], fma(P.Me[h][K], zaa[i], Es[h][i]));
+          }
+      }
+    }
+    // dir 2 (dense): acc[i2] += A2[i2][t2] wMM + M2[i2][t2] wS
+#pragma unroll
+    for (int h = 0; h < K; ++h)
+    {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+      {
+        const int r1 = h, r2 = NI - 1 - h;
+        const T wm1 = h < K - 1 ? Em[h][i] + Om[h][i] : Em[h][i];
+        const T ws1 = h < K - 1 ? Es[h][i] + Os[h][i] : Es[h][i];
+        const T wm2 = h < K - 1 ? Em[h][i] - Om[h][i] : T(0);
+        const T ws2 = h < K - 1 ? Es[h][i] - Os[h][i] : T(0);
+#pragma unroll
+        for (int i2 = 0; i2 < NI; ++i2)
+        {
+          const T cA = D.A[i2][t2], cM = D.M[i2][t2];
+          acc[i2][r1][i] = t2 == 0 ? fma(cA, wm1, cM * ws1) : fma(cA, wm1, fma(cM, ws1, acc[i2][r1][i]));
+          if (h < K - 1)
+            acc[i2][r2][i] = t2 == 0 ? fma(cA, wm2, cM * ws2) : fma(cA, wm2, fma(cM, ws2, acc[i2][r2][i]));
+        }
+      }
+    }
+  }
+  // r = b - acc, then (S x S x S) diag(1/sum lambda) (S x S x S)^T r in registers
+  const T *bb = a.b + (g2 + 1 - a.zoff) * m2 + static_cast<int64_t>(g1 + 1) * m + (g0 + 1);
+#pragma unroll
+  for (int i2 = 0; i2 < NI; ++i2)
+#pragma unroll
+    for (int i1 = 0; i1 < NI; ++i1)
+#pragma unroll
+      for (int i0 = 0; i0 < NI; ++i0)
+        acc[i2][i1][i0] = __ldg(bb + i2 * m2 + i1 * m + i0) - acc[i2][i1][i0];
+  // S^T along dir 2
+#pragma unroll
+  for (int i1 = 0; i1 < NI; ++i1)
+#pragma unroll
+    for (int i0 = 0; i0 < NI; ++i0)
+    {
+      T v[NI], y[NI];
+#pragma unroll
+      for (int i2 = 0; i2 < NI; ++i2)
+        v[i2] = acc[i2][i1][i0];
+      eo_st<K>(P.Se, P.So, v, y);
+#pragma unroll
+      for (int i2 = 0; i2 < NI; ++i2)
+        acc[i2][i1][i0] = y[i2];
+    }
+  // S^T along dir 1
+#pragma unroll
+  for (int c2 = 0; c2 < NI; ++c2)
+#pragma unroll
+    for (int i0 = 0; i0 < NI; ++i0)
+    {
+      T v[NI], y[NI];
+#pragma unroll
+      for (int i1 = 0; i1 < NI; ++i1)
+        v[i1] = acc[c2][i1][i0];
+      eo_st<K>(P.Se, P.So, v, y);
+#pragma unroll
+      for (int i1 = 0; i1 < NI; ++i1)
+        acc[c2][i1][i0] = y[i1];
+    }
+  // dir 0: S^T, scale, S
+#pragma unroll
+  for (int c2 = 0; c2 < NI; ++c2)
+#pragma unroll
+    for (int c1 = 0; c1 < NI; ++c1)
+    {
+      T y[NI];
+      eo_st<K>(P.Se, P.So, acc[c2][c1], y);
+#pragma unroll
+      for (int c0 = 0; c0 < NI; ++c0)
+        y[c0] *= __ldg(a.inv + c0 + NI * (c1 + NI * c2));
+      eo_s<K>(P.Se, P.So, y, acc[c2][c1]);
+    }
+  // S along dir 1
+#pragma unroll
+  for (int c2 = 0; c2 < NI; ++c2)
+#pragma unroll
+    for (int i0 = 0; i0 < NI; ++i0)
+    {
+      T v[NI], y[NI];
+#pragma unroll
+      for (int c1 = 0; c1 < NI; ++c1)
+        v[c1] = acc[c2][c1][i0];
+      eo_s<K>(P.Se, P.So, v, y);
+#pragma unroll
+      for (int i1 = 0; i1 < NI; ++i1)
+        acc[c2][i1][i0] = y[i1];
+    }
+  // S along dir 2, update (x^I_old re-read: only this thread writes it)
+  T *xp = a.x + (g2 + 1 - a.zoff) * m2 + static_cast<int64_t>(g1 + 1) * m + (g0 + 1);
+#pragma unroll
+  for (int i1 = 0; i1 < NI; ++i1)
+#pragma unroll
+    for (int i0 = 0; i0 < NI; ++i0)
+    {
+      T v[NI], y[NI];
+#pragma unroll
+      for (int c2 = 0; c2 < NI; ++c2)
+        v[c2] = acc[c2][i1][i0];
+      eo_s<K>(P.Se, P.So, v, y);
+#pragma unroll
+      for (int i2 = 0; i2 < NI; ++i2)
+      {
+        T *o = xp + i2 * m2 + i1 * m + i0;
+        if constexpr (MODE == MODE_BOUNDARY)
+          *o = y[i2];
+        else
+          *o = __ldg(o) + y[i2];
+      }
+    }
+}
+
+template <int K, typename T, int MODE>
+void launch_vp_patch3d(const PatchMatsEO<T, K> &P, const PatchMats<T, K> &D, const ColorArgs<T> &a,
+                       cudaStream_t s)
+{
+  if (a.total == 0)
+    return;
+  const dim3 block(32, 4, 1);
+  const dim3 grid((a.np[0] + 31) / 32, (a.np[1] + 3) / 4, a.np[2]);
+  pdl_launch(vp_patch3d_kernel<K, T, MODE>, grid, block, 0, s, P, a, D);
+  check_launch("vp_patch3d_kernel");
+}
+
+}  // namespace pmgb

@@ -40,7 +40,7 @@ __all__ = [
     "compute_residual_slab", "restrict_slab", "prolongate_slab",
 ]
 
-_SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2, "sweep": 3}
+_SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2, "sweep": 3, "patch": 4}
 
 
 def set_smoother_impl(impl: str = "auto") -> None:

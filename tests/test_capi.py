@@ -183,7 +183,7 @@ def test_smoother_impl_switch(lib):
     assert lib.pmg_set_smoother_impl(7) != 0
     assert lib.pmg_set_smoother_impl(-1) != 0
     try:
-        for name in ["line", "plane", "sweep", "auto"]:
+        for name in ["line", "plane", "sweep", "patch", "auto"]:
             pmg.set_smoother_impl(name)
             assert pmg.get_smoother_impl() == name
         with pytest.raises(ValueError):

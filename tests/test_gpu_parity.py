@@ -262,7 +262,7 @@ def test_cpp_shim(pmg, cuda):
 # plane-streaming) against the reference, including levels whose colour sizes
 # are not multiples of the patches-per-CTA (ragged last CTA) and level 1
 # (a single patch, the coarse solve).
-@pytest.mark.parametrize("impl", ["auto", "line", "plane", "sweep"])
+@pytest.mark.parametrize("impl", ["auto", "line", "plane", "sweep", "patch"])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 @pytest.mark.parametrize("case", [(2, 1, 1), (2, 1, 6), (2, 2, 1), (2, 2, 3), (2, 2, 6), (2, 3, 1), (2, 3, 5), (3, 1, 1), (3, 1, 5), (3, 2, 1), (3, 2, 3), (3, 2, 5), (3, 3, 1), (3, 3, 4)],
                          ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")

@@ -16,6 +16,8 @@ dim, k, L = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 dtype = sys.argv[4] if len(sys.argv) > 4 else "f64"
 variant = sys.argv[5] if len(sys.argv) > 5 else "fused"
 ns = int(sys.argv[6]) if len(sys.argv) > 6 else 3
+if os.environ.get("PMG_IMPL"):
+    pmg.set_smoother_impl(os.environ["PMG_IMPL"])
 nv = int(sys.argv[7]) if len(sys.argv) > 7 else 0
 dt = np.float64 if dtype == "f64" else np.float32
 tdt = torch.float64 if dtype == "f64" else torch.float32
