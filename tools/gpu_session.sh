@@ -32,10 +32,15 @@ if has sweep; then
         >> "$OUT/sweep3d.jsonl" 2>> "$OUT/sweep.err"
     done
   done
-  for kl in "2 10" "4 9" "7 8"; do
+  for kl in "1 14" "2 13" "3 12" "4 12" "5 11" "6 11" "7 11"; do
     set -- $kl
-    timeout 300 python bench.py --dim 2 --degree $1 --level $2 --dtype f64 --steps 20 --no-cpu \
+    timeout 300 python bench.py --dim 2 --degree $1 --level $2 --dtype f64 --steps 10 --no-cpu \
       >> "$OUT/sweep2d.jsonl" 2>> "$OUT/sweep.err"
+  done
+  for kl in "2 8" "1 9"; do
+    set -- $kl
+    timeout 300 python bench.py --dim 3 --degree $1 --level $2 --dtype f64 --steps 10 --no-cpu \
+      >> "$OUT/sweep3d_big.jsonl" 2>> "$OUT/sweep.err"
   done
   echo "sweep done" >> "$OUT/status.txt"
 fi
@@ -48,7 +53,7 @@ if has full; then
   # the headline config: all 8 colour launches of one step (bench roofline.traffic)
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:vp_ -s 16 -c 8 \
     -o "$OUT/smooth_d3k2L6f64" python tools/prof_target.py 3 2 6 f64 fused 3 > "$OUT/ncu_c2.log" 2>&1
-  for cfg in "3 1 9 f64" "3 4 7 f64" "3 7 6 f64" "3 4 7 f32"; do
+  for cfg in "3 1 9 f64" "3 2 7 f64" "3 4 7 f64" "3 7 6 f64" "3 4 7 f32" "2 2 13 f64"; do
     set -- $cfg
     timeout 600 ncu --set full --clock-control none --import-source on -k regex:vp_ -s 8 -c 1 \
       -o "$OUT/smooth_d$1k$2L$3$4" python tools/prof_target.py $1 $2 $3 $4 fused 2 > "$OUT/ncu_d$1k$2$4.log" 2>&1
