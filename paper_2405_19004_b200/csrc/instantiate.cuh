@@ -19,8 +19,9 @@ namespace pmgb
 namespace
 {
 
-// 3D fused / boundary sweeps of degree <= PMG_PLANE_KMAX use the plane-streaming
-// kernel (smoother_plane.cuh) unless pmg_set_smoother_impl selects the line one
+// 3D fused / boundary sweeps of degree <= PMG_PLANE_KMAX (and f32 degree 3,
+// +7% over the ping-pong kernel) use the plane-streaming kernel
+// (smoother_plane.cuh) unless pmg_set_smoother_impl selects the line one
 #ifndef PMG_PATCH3D_MIN_PATCHES
 #define PMG_PATCH3D_MIN_PATCHES 65536
 #endif
@@ -83,7 +84,7 @@ void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, 
       return;
     }
   }
-  if constexpr (D == 3 && PMG_K <= PMG_PLANE_KMAX)
+  if constexpr (D == 3 && (PMG_K <= PMG_PLANE_KMAX || (PMG_K == 3 && sizeof(T) == 4)))
   {
     if (impl != SMOOTHER_IMPL_LINE && (mode == MODE_FUSED || mode == MODE_BOUNDARY))
     {

@@ -40,7 +40,7 @@ struct PlaneCfg
 #ifndef PMG_PLANE_PB2
 #define PMG_PLANE_PB2 16
 #endif
-  static constexpr int PB = K == 1 ? 64 : PMG_PLANE_PB2;
+  static constexpr int PB = K == 1 ? 64 : (K == 2 ? PMG_PLANE_PB2 : 8);
   // threads: the widest phase (P1: NC per patch, P2/P4: NI^2 per patch)
   static constexpr int LANES = (NC > NI * NI ? NC : NI * NI);
   static constexpr int NT = ((PB * LANES + 31) / 32) * 32;
@@ -49,8 +49,8 @@ struct PlaneCfg
   //   U[p][t2][t1][t0] at p UW + t2 SU2 + t1 SU1 + t0
   //   W: wMM[j][q] at p WW + j SJ + q, wS at p WW + SW + j SJ + q (q = i0 + NI i1);
   //      the eigen-space tensor overwrites wMM in place
-  static constexpr int L64[4][6] = {{0}, {57, 5, 19, 19, 1, 3}, {135, 5, 27, 105, 10, 50}, {0}};
-  static constexpr int L32[4][6] = {{0}, {39, 3, 13, 41, 3, 16}, {145, 5, 29, 105, 10, 50}, {0}};
+  static constexpr int L64[4][6] = {{0}, {57, 5, 19, 19, 1, 3}, {135, 5, 27, 105, 10, 50}, {357, 7, 51, 377, 26, 182}};
+  static constexpr int L32[4][6] = {{0}, {39, 3, 13, 41, 3, 16}, {145, 5, 29, 105, 10, 50}, {371, 7, 53, 409, 28, 197}};
   static constexpr int UW = F64 ? L64[K][0] : L32[K][0];
   static constexpr int SU1 = F64 ? L64[K][1] : L32[K][1];
   static constexpr int SU2 = F64 ? L64[K][2] : L32[K][2];
@@ -351,7 +351,7 @@ __device__ __forceinline__ void plane_tile(const PatchMatsEO<T, K> &P, const Col
 
 // one launch per colour: grid = (ceil(np0 / PB), np1, np2)
 template <int K, typename T, int MODE>
-__global__ void __launch_bounds__(PlaneCfg<K, T>::NT, PMG_PLANE_MINB)
+__global__ void __launch_bounds__(PlaneCfg<K, T>::NT, K == 2 ? PMG_PLANE_MINB : 1)
     vp_smooth_plane_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ ColorArgs<T> a)
 {
   pdl_prologue();
@@ -383,7 +383,7 @@ __device__ __forceinline__ int ld_acquire(const int *p)
 }
 
 template <int K, typename T, int MODE>
-__global__ void __launch_bounds__(PlaneCfg<K, T>::NT, PMG_PLANE_MINB)
+__global__ void __launch_bounds__(PlaneCfg<K, T>::NT, K == 2 ? PMG_PLANE_MINB : 1)
     vp_sweep_plane_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ SweepArgs<T> s)
 {
   pdl_prologue();
