@@ -41,7 +41,10 @@ namespace pmgb
 template <int K, typename T>
 struct Op3Cfg
 {
-  static constexpr int TX = 32, TY = 8, NT = TX * TY, W = 2 * K + 1;
+#ifndef PMG_OP_TY
+#define PMG_OP_TY 8
+#endif
+  static constexpr int TX = 32, TY = PMG_OP_TY, NT = TX * TY, W = 2 * K + 1;
   static constexpr int XW = TX + 2 * K, XH = TY + 2 * K, XN = XW * XH;
   static constexpr int NLOAD = (XN + NT - 1) / NT;   // tile slots per thread
   static constexpr int ROWS = (XH + TY - 1) / TY;    // dir-0 rows per thread
