@@ -229,6 +229,20 @@ void level_init(pmg_level_s *l)
     // the dir-2 contraction of the one-thread-per-patch 3D kernel
     for (const Dense *dm : {&S.mass_if, &S.stiff_if, &S.S})
       v.insert(v.end(), dm->a.begin(), dm->a.end());
+    // S^T M_if and S^T A_if (eigen rows in the even-first order): the 3D
+    // one-thread-per-patch kernel applies dir 2 and the first S^T in one step
+    {
+      const int ni = 2 * S.k - 1, nc = 2 * S.k + 1;
+      for (const Dense *dm : {&S.mass_if, &S.stiff_if})
+        for (int c = 0; c < ni; ++c)
+          for (int t = 0; t < nc; ++t)
+          {
+            double acc = 0.0;
+            for (int i = 0; i < ni; ++i)
+              acc += S.S(i, S.eo_perm[c]) * (*dm)(i, t);
+            v.push_back(static_cast<T>(acc));
+          }
+    }
     l->patch_mats.resize(v.size() * sizeof(T));
     std::memcpy(l->patch_mats.data(), v.data(), l->patch_mats.size());
   }

@@ -74,9 +74,9 @@ void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, 
     if ((impl == SMOOTHER_IMPL_PATCH || (impl == SMOOTHER_IMPL_AUTO && big)) &&
         (mode == MODE_FUSED || mode == MODE_BOUNDARY))
     {
-      // dense PatchMats after the even-odd matrices in the parameter blob
-      const auto &DM = *reinterpret_cast<const PatchMats<T, PMG_K> *>(static_cast<const unsigned char *>(P) +
-                                                                      sizeof(PatchMatsEO<T, PMG_K>));
+      // S^T M_if, S^T A_if after the even-odd and dense matrices in the parameter blob
+      const auto &DM = *reinterpret_cast<const PatchST<T, PMG_K> *>(
+          static_cast<const unsigned char *>(P) + sizeof(PatchMatsEO<T, PMG_K>) + sizeof(PatchMats<T, PMG_K>));
       if (mode == MODE_FUSED)
         launch_vp_patch3d<PMG_K, T, MODE_FUSED>(PM, DM, a, s);
       else

@@ -272,10 +272,18 @@ namespace pmgb
 // densely into the NI^3 residual; then the 3D fast-diagonalisation solve in
 // registers and the x^I update. No shared memory, no barriers.
 // ---------------------------------------------------------------------------
+// S^T M_if, S^T A_if with eigen rows in the even-first order (capi.cu level_init)
+template <typename T, int K>
+struct PatchST
+{
+  T M[2 * K - 1][2 * K + 1];
+  T A[2 * K - 1][2 * K + 1];
+};
+
 template <int K, typename T, int MODE>
 __global__ void __launch_bounds__(128, 3) vp_patch3d_kernel(const __grid_constant__ PatchMatsEO<T, K> P,
                                                             const __grid_constant__ ColorArgs<T> a,
-                                                            const __grid_constant__ PatchMats<T, K> D)
+                                                            const __grid_constant__ PatchST<T, K> D)
 {
   constexpr int NC = 2 * K + 1, NI = 2 * K - 1;
   constexpr int HO = K > 1 ? K - 1 : 1;
@@ -357,7 +365,7 @@ __global__ void __launch_bounds__(128, 3) vp_patch3d_kernel(const __grid_constan
           }
       }
     }
-    // dir 2 (dense): acc[i2] += A2[i2][t2] wMM + M2[i2][t2] wS
+    // dir 2 and S^T along dir 2 in one step: acc[c2] += (S^T A2)[c2][t2] wMM + (S^T M2)[c2][t2] wS
 #pragma unroll
     for (int h = 0; h < K; ++h)
     {
@@ -380,16 +388,8 @@ __global__ void __launch_bounds__(128, 3) vp_patch3d_kernel(const __grid_constan
       }
     }
   }
-  // r = b - acc, then (S x S x S) diag(1/sum lambda) (S x S x S)^T r in registers
+  // S^T_2 r = S^T_2 b - acc, then the rest of (S x S x S) diag(1/sum lambda) (S x S x S)^T r
   const T *bb = a.b + (g2 + 1 - a.zoff) * m2 + static_cast<int64_t>(g1 + 1) * m + (g0 + 1);
-#pragma unroll
-  for (int i2 = 0; i2 < NI; ++i2)
-#pragma unroll
-    for (int i1 = 0; i1 < NI; ++i1)
-#pragma unroll
-      for (int i0 = 0; i0 < NI; ++i0)
-        acc[i2][i1][i0] = __ldg(bb + i2 * m2 + i1 * m + i0) - acc[i2][i1][i0];
-  // S^T along dir 2
 #pragma unroll
   for (int i1 = 0; i1 < NI; ++i1)
 #pragma unroll
@@ -398,11 +398,11 @@ __global__ void __launch_bounds__(128, 3) vp_patch3d_kernel(const __grid_constan
       T v[NI], y[NI];
 #pragma unroll
       for (int i2 = 0; i2 < NI; ++i2)
-        v[i2] = acc[i2][i1][i0];
+        v[i2] = __ldg(bb + i2 * m2 + i1 * m + i0);
       eo_st<K>(P.Se, P.So, v, y);
 #pragma unroll
-      for (int i2 = 0; i2 < NI; ++i2)
-        acc[i2][i1][i0] = y[i2];
+      for (int c2 = 0; c2 < NI; ++c2)
+        acc[c2][i1][i0] = y[c2] - acc[c2][i1][i0];
     }
   // S^T along dir 1
 #pragma unroll
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(128, 3) vp_patch3d_kernel(const __grid_constan
 }
 
 template <int K, typename T, int MODE>
-void launch_vp_patch3d(const PatchMatsEO<T, K> &P, const PatchMats<T, K> &D, const ColorArgs<T> &a,
+void launch_vp_patch3d(const PatchMatsEO<T, K> &P, const PatchST<T, K> &D, const ColorArgs<T> &a,
                        cudaStream_t s)
 {
   if (a.total == 0)
