@@ -286,7 +286,8 @@ def main():
         x = torch.rand(plan.nplanes * plan.plane_size, dtype=tdt, device="cuda", generator=gen) * 2 - 1
         b = torch.rand(plan.nplanes * plan.plane_size, dtype=tdt, device="cuda", generator=gen) * 2 - 1
         comm = dd.StagedComm(x, plan.plane_size) if shared else dd.TorchDistComm(x, plan.plane_size)
-        smoother = dd.SlabSmoother(plan, dd.gpu_kernel(lev, plan, x, b, args.variant), comm)
+        smoother = dd.SlabSmoother(plan, dd.gpu_kernel(lev, plan, x, b, args.variant), comm,
+                                   side_stream=None if shared else torch.cuda.Stream())
 
         def step():
             smoother.smooth()

@@ -136,24 +136,44 @@ class SlabSmoother:
     recvs carry (peer, first local plane, nplanes).
     """
 
-    def __init__(self, plan: SlabPlan, kernel, comm):
+    def __init__(self, plan: SlabPlan, kernel, comm, side_stream=None):
         self.plan, self.kernel, self.comm = plan, kernel, comm
         self.steps = [colour_step(plan, c) for c in range(8)]
+        # optional torch.cuda.Stream: the boundary-layer patches and the plane
+        # messages run on it, concurrently with the interior patches on the
+        # current stream (they are independent patches of the same colour)
+        self.side = side_stream
 
     def smooth(self):
         p = self.plan
+        if self.side is not None:
+            import torch
         for c in range(8):
             st = self.steps[c]
-            for lo, hi in st.early:
-                self.kernel(c, lo, hi)
+            sends = [(q, g0 - p.lo, n) for q, g0, n in st.sends]
+            recvs = [(q, g0 - p.lo, n) for q, g0, n in st.recvs]
             h = None
-            if st.sends or st.recvs:
-                h = self.comm.post([(q, g0 - p.lo, n) for q, g0, n in st.sends],
-                                   [(q, g0 - p.lo, n) for q, g0, n in st.recvs])
+            if self.side is None:
+                for lo, hi in st.early:
+                    self.kernel(c, lo, hi)
+                if sends or recvs:
+                    h = self.comm.post(sends, recvs)
+                for lo, hi in st.late:
+                    self.kernel(c, lo, hi)
+                if h is not None:
+                    h.wait()
+                continue
+            main = torch.cuda.current_stream()
+            self.side.wait_stream(main)
+            with torch.cuda.stream(self.side):
+                for lo, hi in st.early:
+                    self.kernel(c, lo, hi)
+                if sends or recvs:
+                    h = self.comm.post(sends, recvs)
+                    h.wait()
             for lo, hi in st.late:
                 self.kernel(c, lo, hi)
-            if h is not None:
-                h.wait()
+            main.wait_stream(self.side)
 
 
 class TorchDistComm:

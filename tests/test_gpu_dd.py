@@ -84,3 +84,59 @@ def test_slab_vcycle_bitwise(tmp_path, world, k, level, dtype):
     mp.spawn(_worker, args=(world, _free_port(), k, level, dtype, out), nprocs=world, join=True)
     same, err, scale, agg = np.load(out)
     assert same == 1.0, (err, scale, agg)
+
+
+def _smoother_worker(rank, world, port, k, level, stack, out_path):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_19004_b200 as pmg
+    from paper_2405_19004_b200 import dd
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        mg = pmg.make_multigrid_context(3, k, level, dtype=np.float64)
+        lev = mg.levels[-1]
+        full = dd.make_plan(1, 0, k, level, stack)
+        n = full.nplanes * full.plane_size
+        rng = np.random.default_rng(51)
+        x0 = torch.from_numpy(rng.uniform(-1, 1, n)).cuda()
+        b = torch.from_numpy(rng.uniform(-1, 1, n)).cuda()
+        plan = dd.make_plan(world, rank, k, level, stack)
+        x = dd.scatter_global(plan, x0).clone()
+        bl = dd.scatter_global(plan, b).clone()
+        sm = dd.SlabSmoother(plan, dd.gpu_kernel(lev, plan, x, bl), dd.StagedComm(x, plan.plane_size),
+                             side_stream=torch.cuda.Stream())
+        for _ in range(2):
+            sm.smooth()
+        torch.cuda.synchronize()
+        own = dd.owned_part(plan, x).cpu()
+        sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([own.numel()]))
+        mx = int(max(s.item() for s in sizes))
+        padded = torch.zeros(mx, dtype=own.dtype)
+        padded[: own.numel()] = own
+        parts = [torch.zeros(mx, dtype=own.dtype) for _ in sizes]
+        dist.all_gather(parts, padded)
+        if rank == 0:
+            got = torch.cat([p[: int(s.item())] for p, s in zip(parts, sizes)]).numpy()
+            xg = x0.clone()
+            for _ in range(2):
+                dd.virtual_smooth([full], [dd.gpu_kernel(lev, full, xg, b)], [xg])
+            want = xg.cpu().numpy()
+            np.save(out_path, np.array([float(np.array_equal(got, want)), np.abs(got - want).max()]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k,level,stack", [(2, 2, 5, 1), (2, 3, 4, 2), (3, 2, 4, 3)])
+def test_slab_smoother_side_stream_bitwise(tmp_path, world, k, level, stack):
+    """SlabSmoother with the boundary-layer patches and plane messages on a
+    side stream (the NCCL bench path's organisation) == one domain, bitwise."""
+    out = str(tmp_path / "res.npy")
+    mp.spawn(_smoother_worker, args=(world, _free_port(), k, level, stack, out), nprocs=world, join=True)
+    same, err = np.load(out)
+    assert same == 1.0, err
