@@ -365,3 +365,20 @@ def test_device_rhs_and_l2(pmg, cuda, case):
     got32 = cuda.empty(lev.level.total_dofs, dtype=cuda.float32, device="cuda")
     pmg.compute_rhs_device(ctx32.levels[-1], "sin", got32)
     assert rel(got32.cpu().numpy(), refbind.compute_rhs(dim, k, L, 1)) < 1e-6
+
+
+# The size-dependent default: 3D k = 2 colours with >= 65536 patches run one
+# thread per patch (vp_patch3d_kernel). One level large enough to select it,
+# against the reference (multi-threaded CPU), f64 and f32, fused and boundary.
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_large_level_default_kernels(pmg, cuda, dtype):
+    dim, k, L = 3, 2, 7
+    ref = refbind.RefMg(dim, k, L, prec=0 if dtype == np.float64 else 1, threads=8)
+    ctx = pmg.make_multigrid_context(dim, k, L, dtype=dtype)
+    lev = ctx.levels[-1]
+    x0, b = inputs(lev.level.total_dofs, dtype, seed=5)
+    for variant in ["fused", "boundary"]:
+        xd = dev(cuda, x0.copy())
+        pmg.smooth(lev, xd, dev(cuda, b), variant)
+        want = ref.smooth(L - 1, x0, b, variant)
+        assert rel(xd.cpu().numpy(), want) < TOL[dtype], (variant, rel(xd.cpu().numpy(), want))
