@@ -189,7 +189,7 @@ def smoother_kernel_name(args):
     if args.dim == 3 and args.degree == 2:
         per_colour = ((1 << args.level) - 1) ** 3 / 8
         return "vp_patch3d_kernel" if per_colour >= 65536 else "vp_smooth_plane_kernel"
-    if args.dim == 2 and args.degree in (2, 3):
+    if args.dim == 2 and (args.degree in (2, 3) or (args.degree == 4 and args.dtype == "f32")):
         return "vp_patch2d_kernel"
     if args.dim == 3 and args.degree == 3 and args.dtype == "f32":
         return "vp_smooth_plane_kernel"

@@ -52,7 +52,7 @@ void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, 
       return;
     }
   }
-  if constexpr (D == 2 && PMG_K >= 2 && PMG_K <= PMG_PATCH2D_KMAX)
+  if constexpr (D == 2 && PMG_K >= 2 && (PMG_K <= PMG_PATCH2D_KMAX || (PMG_K == 4 && sizeof(T) == 4)))
   {
     // 2D degree 2..: one thread per patch, all in registers (smoother_patch2d.cuh)
     if (impl != SMOOTHER_IMPL_LINE && (mode == MODE_FUSED || mode == MODE_BOUNDARY))
