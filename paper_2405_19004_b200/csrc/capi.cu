@@ -461,10 +461,10 @@ void prolongate_impl(pmg_level_s *c, pmg_level_s *f, const T *xc, T *xf, bool ac
 }
 
 template <typename T>
-void restrict_impl(pmg_level_s *c, pmg_level_s *f, const T *rf, T *rc, cudaStream_t s)
+void restrict_impl(pmg_level_s *c, pmg_level_s *f, const T *rf, T *rc, cudaStream_t s, T *zero = nullptr)
 {
   transfer_scratch<T>(f);
-  ktab<T>(f).restrict_(f->prol_mats.data(), rf, rc, c->S.m, f->tA.as<T>(), f->tB.as<T>(),
+  ktab<T>(f).restrict_(f->prol_mats.data(), rf, rc, zero, c->S.m, f->tA.as<T>(), f->tB.as<T>(),
                        f->sm_count, s);
 }
 
@@ -498,9 +498,8 @@ void vcycle_impl(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s)
   T *bc = mg->bc_ws[li]->as<T>();
   T *xc = mg->xc_ws[li]->as<T>();
   ktab<T>(lev).level_op(lev->band_mats.data(), x, b, r, lev->S.m, lev->sm_count, s);
-  restrict_impl<T>(crs, lev, r, bc, s);
-  if (li - 1 > 0)
-    launch_fill<T>(xc, crs->S.N, T(0), crs->sm_count, s);  // the coarse solve zeroes x itself
+  // b_c = R r and x_c = 0 in the same launch (the coarse solve zeroes x itself)
+  restrict_impl<T>(crs, lev, r, bc, s, li - 1 > 0 ? xc : nullptr);
   vcycle_impl<T>(mg, li - 1, xc, bc, s);
   prolongate_impl<T>(crs, lev, xc, x, true, s);
   for (int i = 0; i < mg->post; ++i)

@@ -29,7 +29,8 @@ struct KernelTable
   // P: ProlMats<T,K>*
   void (*prolongate)(const void *P, const T *xc, T *xf, bool acc, int64_t mc, T *tA, T *tB,
                      int sm_count, cudaStream_t s) = nullptr;
-  void (*restrict_)(const void *P, const T *rf, T *rc, int64_t mc, T *tA, T *tB, int sm_count,
+  // zero (optional): cleared at the coarse nodes (the V-cycle's x_c = 0)
+  void (*restrict_)(const void *P, const T *rf, T *rc, T *zero, int64_t mc, T *tA, T *tB, int sm_count,
                     cudaStream_t s) = nullptr;
   size_t smooth_smem = 0;   // dynamic smem per CTA of the fused kernel
   int smooth_threads = 0;   // threads per CTA

@@ -145,10 +145,10 @@ void prol_entry(const void *P, const T *xc, T *xf, bool acc, int64_t mc, T *tA, 
 }
 
 template <int D, typename T>
-void rest_entry(const void *P, const T *rf, T *rc, int64_t mc, T *tA, T *tB, int sm_count,
+void rest_entry(const void *P, const T *rf, T *rc, T *zero, int64_t mc, T *tA, T *tB, int sm_count,
                 cudaStream_t s)
 {
-  launch_restrict<D, PMG_K, T>(*static_cast<const ProlMats<T, PMG_K> *>(P), rf, rc, mc, tA, tB,
+  launch_restrict<D, PMG_K, T>(*static_cast<const ProlMats<T, PMG_K> *>(P), rf, rc, zero, mc, tA, tB,
                                sm_count, s);
 }
 

@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(256)
 template <int K, typename T, int DIR>
 __global__ void __launch_bounds__(256)
     restrict_pass_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ in,
-                         T *__restrict__ out, int64_t e0, int64_t e1, int64_t e2, int64_t mf, int64_t z0)
+                         T *__restrict__ out, int64_t e0, int64_t e1, int64_t e2, int64_t mf, int64_t z0,
+                         T *__restrict__ zero = nullptr)
 {
   pdl_prologue();
   __shared__ T Ps[2 * K + 1][K + 1];
@@ -128,6 +129,8 @@ __global__ void __launch_bounds__(256)
     }
   }
   out[(i2 * e1 + i1) * e0 + i0] = s;
+  if (zero)
+    zero[(i2 * e1 + i1) * e0 + i0] = T(0);
 }
 
 // PMG_TRANSFER_PASSES=1 selects the separate 1D passes (A/B measurement)
@@ -250,6 +253,170 @@ __global__ void __launch_bounds__(Prol3Cfg<K>::NT)
   }
 }
 
+// ---------------------------------------------------------------------------
+// 3D restriction in one kernel, marching along z. CTA = OX x OY coarse
+// columns (whole coarse cells: OX = CX K, OY = CY K) and a range of coarse
+// z-nodes [Qa, Qb]. Per fine z-plane of the cells that touch the range: the
+// (WY x WX) fine window of the tile (2K (C+1) fine nodes per direction, the
+// cells c0 .. c0 + C) is staged by cp.async (double-buffered, zero-filled
+// past the last fine node), the x pass gathers it to R1[WY][OX] in shared
+// memory, the y pass gives each thread its (qx, qy) value v of this plane,
+// and the z pass accumulates P[r][t] v into K + 1 registers of the current
+// cell. Nodes t = 1 .. K-1 of a cell are complete when the cell ends; node
+// t = 0 adds the t = K partial of the previous cell (a register carry).
+// Traffic: r_f once (+ the x / y window halo and one extra cell per z chunk)
+// and R r_f once, against ~2.6 N words for the three 1D passes; one launch
+// instead of three. `zero` (optional) is cleared at the output nodes (the
+// V-cycle's x_c = 0).
+// ---------------------------------------------------------------------------
+template <int K>
+struct Rest3Cfg
+{
+  static constexpr int CX = 32 / K, CY = (8 / K) >= 2 ? 8 / K : (K <= 5 ? 2 : 1);  // static smem <= 48 KB
+  static constexpr int OX = CX * K, OY = CY * K;
+  static constexpr int WX = 2 * K * (CX + 1), WY = 2 * K * (CY + 1), WN = WX * WY;
+  static constexpr int NT = 32 * OY;
+  static constexpr int NLOAD = (WN + NT - 1) / NT;
+};
+
+template <typename T>
+__device__ __forceinline__ void tr_cp_async(T *smem, const T *gmem, bool valid)
+{
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 4 : 0)
+                 : "memory");
+}
+
+// coarse node Q (1-based, one direction) = sum over its <= 2 cells (c, t) and
+// r = 1..2K of P[r][t] fine(2cK + r); here as offsets into a window whose
+// first fine node is 2 c0 K + 1
+template <int K, typename T, typename F>
+__device__ __forceinline__ T rest_gather_1d(const T (*Ps)[K + 1], int Q, int c0, F &&fine)
+{
+  const int tq = Q % K, c1 = Q / K;
+  T s = T(0);
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+  {
+    if (h == 1 && tq != 0)
+      break;
+    const int c = tq == 0 ? c1 - 1 + h : c1;
+    const int t = tq == 0 ? (h == 0 ? K : 0) : tq;
+    const int base = 2 * (c - c0) * K - 1;  // window offset of fine node r = 0 of cell c
+#pragma unroll
+    for (int r = 1; r <= 2 * K; ++r)
+      s = fma(Ps[r][t], fine(base + r), s);
+  }
+  return s;
+}
+
+template <int K, typename T>
+__global__ void __launch_bounds__(Rest3Cfg<K>::NT)
+    restrict3d_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ rf, T *__restrict__ rc,
+                      T *__restrict__ zero, int mc, int q0, int q1, int nodes_per_chunk)
+{
+  using C = Rest3Cfg<K>;
+  constexpr int CX = C::CX, CY = C::CY, OX = C::OX, OY = C::OY, WX = C::WX, WY = C::WY, NT = C::NT;
+  __shared__ T Ps[2 * K + 1][K + 1];
+  __shared__ __align__(16) T F[2][WY * WX];
+  __shared__ T R1[WY][OX];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  for (int e = tid; e < (2 * K + 1) * (K + 1); e += NT)
+    (&Ps[0][0])[e] = (&P.P[0][0])[e];
+  const int mf = 2 * mc + 1;
+  const int cx0 = blockIdx.x * CX, cy0 = blockIdx.y * CY;
+  // owned coarse z-nodes [Qa, Qb] (1-based) and the cells that touch them
+  const int Qa = q0 + 1 + blockIdx.z * nodes_per_chunk;
+  const int Qb = min(q1, q0 + (static_cast<int>(blockIdx.z) + 1) * nodes_per_chunk);
+  const int c_lo = (Qa % K == 0) ? Qa / K - 1 : Qa / K, c_hi = Qb / K;
+  // fixed staging slots of this thread: window element -> (fy, fx)
+  const int64_t mf2 = static_cast<int64_t>(mf) * mf;
+  const T *wbase = rf + static_cast<int64_t>(2 * cy0 * K) * mf + 2 * cx0 * K;  // fine (p_y, p_x) = window (0, 0)
+  int goff[C::NLOAD];
+  bool gok[C::NLOAD];
+#pragma unroll
+  for (int j = 0; j < C::NLOAD; ++j)
+  {
+    const int e = tid + j * NT;
+    const int fy = e / WX, fx = e - fy * WX;
+    gok[j] = e < C::WN && 2 * cy0 * K + fy < mf && 2 * cx0 * K + fx < mf;
+    goff[j] = gok[j] ? fy * mf + fx : 0;
+  }
+  auto stage = [&](int buf, int pz) {  // pz: 0-based fine plane
+    const bool zok = pz < mf;
+    const T *src = wbase + (zok ? static_cast<int64_t>(pz) * mf2 : 0);
+#pragma unroll
+    for (int j = 0; j < C::NLOAD; ++j)
+    {
+      const int e = tid + j * NT;
+      if (e < C::WN)
+        tr_cp_async(&F[buf][e], src + goff[j], gok[j] && zok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  pdl_prologue();
+  __syncthreads();  // Ps
+  const int qx = cx0 * K + 1 + tx, qy = cy0 * K + 1 + ty;  // this thread's coarse column (y pass)
+  const bool own = tx < OX && qx <= mc && qy <= mc;
+  T acc[K + 1], carry = T(0);
+  const int nplanes = (c_hi - c_lo + 1) * 2 * K;
+  stage(0, 2 * c_lo * K);
+  int s = 0;
+  for (int cz = c_lo; cz <= c_hi; ++cz)
+  {
+#pragma unroll
+    for (int t = 0; t <= K; ++t)
+      acc[t] = T(0);
+#pragma unroll
+    for (int r = 1; r <= 2 * K; ++r, ++s)
+    {
+      const int buf = s & 1;
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
+      if (s + 1 < nplanes)
+        stage(buf ^ 1, 2 * cz * K + r);  // next plane: 0-based index of lattice 2czK + r + 1
+      // x pass: R1[fy][ox] for the tile's coarse x nodes
+      if (tx < OX)
+      {
+        const T *Fb = F[buf];
+        for (int fy = ty; fy < WY; fy += OY)
+          R1[fy][tx] = rest_gather_1d<K, T>(Ps, qx, cx0, [&](int o) { return Fb[fy * WX + o]; });
+      }
+      __syncthreads();
+      if (tx < OX)
+      {
+        const T v = rest_gather_1d<K, T>(Ps, qy, cy0, [&](int o) { return R1[o][tx]; });
+#pragma unroll
+        for (int t = 0; t <= K; ++t)
+          acc[t] = fma(Ps[r][t], v, acc[t]);
+      }
+    }
+    // complete nodes: cz K (t = 0, plus the previous cell's t = K) and cz K + t
+    if (own)
+    {
+      T *o = rc + static_cast<int64_t>(qy - 1) * mc + (qx - 1);
+      T *z = zero ? zero + static_cast<int64_t>(qy - 1) * mc + (qx - 1) : nullptr;
+#pragma unroll
+      for (int t = 0; t < K; ++t)
+      {
+        const int Q = cz * K + t;
+        if (Q >= Qa && Q <= Qb && Q >= 1)
+        {
+          const int64_t off = static_cast<int64_t>(Q - 1) * mc * mc;
+          o[off] = t == 0 ? carry + acc[0] : acc[t];
+          if (z)
+            z[off] = T(0);
+        }
+      }
+    }
+    carry = acc[K];
+  }
+}
+
 template <int D, int K, typename T>
 void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, int64_t mc,
                        T *tA, T *tB, int sm_count, cudaStream_t s)
@@ -292,25 +459,64 @@ void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, in
   }
 }
 
+// Where the z-march wins (tools/quick_ops.py, profiles/r01/restrict3d.txt):
+// k = 1, 2, 4 on fine levels of >= 96 nodes per direction (1.3-1.6x over the
+// passes). Below that the per-plane staging latency of the march (2k planes
+// per cell in sequence) exceeds three fully parallel passes; for k = 3, 5-7
+// the y-window halo (CY = 2 or 1 cells) costs more than the saved traffic.
+template <int K>
+inline bool use_restrict3d(int64_t mc)
+{
+  return use_fused_transfer() && (K == 1 || K == 2 || K == 4) && 2 * mc + 1 >= 96;
+}
+
+// coarse z-nodes [q0, q1) (0-based) of R r_f in one launch; chunks of the
+// node range along z so that ~4 CTAs per SM are in flight
+template <int K, typename T>
+void launch_restrict3d(const ProlMats<T, K> &P, const T *rf, T *rc, T *zero, int64_t mc, int64_t q0, int64_t q1,
+                       int sm_count, cudaStream_t s)
+{
+  using C = Rest3Cfg<K>;
+  const int64_t gx = (mc + C::OX - 1) / C::OX, gy = (mc + C::OY - 1) / C::OY;
+  const int64_t nq = q1 - q0;
+  const int64_t want = std::max<int64_t>(1, (4 * static_cast<int64_t>(sm_count)) / (gx * gy));
+  const int64_t cells = (nq + K - 1) / K;
+  const int64_t chunks = std::min<int64_t>(want, cells);
+  const int64_t npc = ((cells + chunks - 1) / chunks) * K;  // nodes per chunk (whole cells)
+  const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>((nq + npc - 1) / npc));
+  pdl_launch(restrict3d_kernel<K, T>, grid, dim3(32, C::OY), 0, s, P, rf, rc, zero, static_cast<int>(mc),
+             static_cast<int>(q0), static_cast<int>(q1), static_cast<int>(npc));
+  check_launch("restrict3d_kernel");
+}
+
 template <int D, int K, typename T>
-void launch_restrict(const ProlMats<T, K> &P, const T *rf, T *rc, int64_t mc, T *tA, T *tB,
+void launch_restrict(const ProlMats<T, K> &P, const T *rf, T *rc, T *zero, int64_t mc, T *tA, T *tB,
                      int sm_count, cudaStream_t s)
 {
   const int64_t mf = 2 * mc + 1;
   if constexpr (D == 2)
   {
-    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, 1), dim3(32, 8), 0, s, P, rf, tA, mc, mf, 1, mf, int64_t(0));
+    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, 1), dim3(32, 8), 0, s, P, rf, tA, mc, mf, 1, mf, int64_t(0),
+               static_cast<T *>(nullptr));
     check_launch("restrict_pass0");
-    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, 1), dim3(32, 8), 0, s, P, tA, rc, mc, mc, 1, mf, int64_t(0));
+    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, 1), dim3(32, 8), 0, s, P, tA, rc, mc, mc, 1, mf, int64_t(0),
+               zero);
     check_launch("restrict_pass1");
+  }
+  else if (use_restrict3d<K>(mc))
+  {
+    launch_restrict3d<K, T>(P, rf, rc, zero, mc, 0, mc, sm_count, s);
   }
   else
   {
-    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, mf), dim3(32, 8), 0, s, P, rf, tA, mc, mf, mf, mf, int64_t(0));
+    pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, mf), dim3(32, 8), 0, s, P, rf, tA, mc, mf, mf, mf, int64_t(0),
+               static_cast<T *>(nullptr));
     check_launch("restrict_pass0");
-    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, mf), dim3(32, 8), 0, s, P, tA, tB, mc, mc, mf, mf, int64_t(0));
+    pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, mf), dim3(32, 8), 0, s, P, tA, tB, mc, mc, mf, mf, int64_t(0),
+               static_cast<T *>(nullptr));
     check_launch("restrict_pass1");
-    pdl_launch(restrict_pass_kernel<K, T, 2>, pass_grid(mc, mc, mc), dim3(32, 8), 0, s, P, tB, rc, mc, mc, mc, mf, int64_t(0));
+    pdl_launch(restrict_pass_kernel<K, T, 2>, pass_grid(mc, mc, mc), dim3(32, 8), 0, s, P, tB, rc, mc, mc, mc, mf, int64_t(0),
+               zero);
     check_launch("restrict_pass2");
   }
 }
@@ -359,17 +565,22 @@ void launch_restrict_slab(const ProlMats<T, K> &P, const T *rf, T *rc, int64_t m
 {
   if (q1 <= q0)
     return;
+  if (use_restrict3d<K>(mc))
+  {
+    launch_restrict3d<K, T>(P, rf, rc, static_cast<T *>(nullptr), mc, q0, q1, 148, s);
+    return;
+  }
   const int64_t mf = 2 * mc + 1;
   int64_t pz0, pz1;
   restrict_slab_fine_range(K, mc, q0, q1, pz0, pz1);
   pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, pz1 - pz0), dim3(32, 8), 0, s, P, rf, tA, mc, mf, mf,
-             mf, pz0);
+             mf, pz0, static_cast<T *>(nullptr));
   check_launch("restrict_pass0(slab)");
   pdl_launch(restrict_pass_kernel<K, T, 1>, pass_grid(mc, mc, pz1 - pz0), dim3(32, 8), 0, s, P, tA, tB, mc, mc, mf,
-             mf, pz0);
+             mf, pz0, static_cast<T *>(nullptr));
   check_launch("restrict_pass1(slab)");
   pdl_launch(restrict_pass_kernel<K, T, 2>, pass_grid(mc, mc, q1 - q0), dim3(32, 8), 0, s, P, tB, rc, mc, mc, mc,
-             mf, q0);
+             mf, q0, static_cast<T *>(nullptr));
   check_launch("restrict_pass2(slab)");
 }
 

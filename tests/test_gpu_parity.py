@@ -382,3 +382,23 @@ def test_large_level_default_kernels(pmg, cuda, dtype):
         pmg.smooth(lev, xd, dev(cuda, b), variant)
         want = ref.smooth(L - 1, x0, b, variant)
         assert rel(xd.cpu().numpy(), want) < TOL[dtype], (variant, rel(xd.cpu().numpy(), want))
+
+
+# restrict3d_kernel (the z-marching restriction) is selected for k = 1, 2, 4
+# on fine levels of >= 96 nodes per direction; the cases above are smaller
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", [(3, 1, 7), (3, 2, 6), (3, 4, 5)], ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")
+def test_restrict3d_large(pmg, cuda, case, dtype):
+    dim, k, L = case
+    ref = refbind.RefMg(dim, k, L, prec=0 if dtype == np.float64 else 1)
+    ctx = pmg.make_multigrid_context(dim, k, L, dtype=dtype)
+    c, f = ctx.levels[-2], ctx.levels[-1]
+    rf, _ = inputs(f.level.total_dofs, dtype, seed=9)
+    rc = cuda.zeros(c.level.total_dofs, dtype=cuda.float64 if dtype == np.float64 else cuda.float32, device="cuda")
+    pmg.restrict_vector(c, f, dev(cuda, rf), rc)
+    assert rel(rc.cpu().numpy(), ref.restrict(L - 2, rf)) < TOL[dtype]
+    if dtype == np.float64 and k == 2:
+        x0, b = inputs(f.level.total_dofs, dtype)
+        xd = dev(cuda, x0.copy())
+        pmg.v_cycle(ctx, L - 1, xd, dev(cuda, b))
+        assert rel(xd.cpu().numpy(), ref.vcycle(L - 1, x0, b)) < 1e-11
