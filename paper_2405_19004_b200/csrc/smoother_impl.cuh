@@ -136,6 +136,24 @@ __device__ __forceinline__ void cp_async_elem(T *smem, const T *gmem, bool valid
                  "r"(valid ? 4 : 0)
                  : "memory");
 }
+// same, destination given as a shared-window address (callers advance it by
+// compile-time offsets instead of converting a generic pointer per element)
+template <typename T>
+__device__ __forceinline__ void cp_async_sa(unsigned s, const T *gmem, bool valid)
+{
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ unsigned smem_addr(const void *p)
+{
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -373,6 +391,23 @@ __global__ void __launch_bounds__(sm_nt<D, K, T>(), sm_minb<D, K, T>())
     const int64_t base = (D == 3) ? static_cast<int64_t>(y1) * m + y0 : static_cast<int64_t>(y0);
     const int64_t zl = (D == 3) ? a.zoff : 0;
     const int64_t mlast = (D == 3) ? a.mz : m;
+    if constexpr (sizeof(T) == 4)
+    {
+      // f32 (issue-bound): addresses advanced per line, range as two int compares
+      const int tlo = -ylast0, thi = mlast - ylast0 < NC ? static_cast<int>(mlast - ylast0) : NC;
+      const T *src = inplane ? a.x + base + (ylast0 - zl) * step : a.x;
+      const unsigned sdst = smem_addr(U + p * UW + rr);
+#pragma unroll
+      for (int t = 0; t < NC; ++t)
+      {
+        bool ok = inplane && t >= tlo && t < thi;
+        if constexpr (MODE == MODE_BOUNDARY)
+          ok = ok && !(t0 >= 1 && t0 <= NC - 2 && t >= 1 && t <= NC - 2 && (D == 2 || (t1 >= 1 && t1 <= NC - 2)));
+        cp_async_sa<T>(sdst + static_cast<unsigned>(sizeof(T) * (D == 3 ? NC * NC : NC) * t), src, ok);
+        src += step;
+      }
+      return;
+    }
     T *dst = U + p * UW + rr;
 #pragma unroll
     for (int t = 0; t < NC; ++t)
