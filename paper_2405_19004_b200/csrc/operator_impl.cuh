@@ -79,6 +79,49 @@ constexpr int op3d_minb()
   return K >= 3 ? 2 : 1;
 }
 
+// dir 1 for a warp whose rows have lattice residue RES: rows of residue
+// RES != 0 couple only their own cell (band offsets [K - RES, 2K - RES]), so
+// the structurally zero taps, and their shared-memory loads, are dropped at
+// compile time (bitwise the same sums: the dropped terms are exact zeros)
+template <int K, typename T, int RES>
+__device__ __forceinline__ void op3_dir1(const T *zm, const T *za, const T *cm_, const T *ca_, int wy, int lane,
+                                         T &wm_out, T &ws_out)
+{
+  constexpr int W = 2 * K + 1, TX = 32;
+  T wm = T(0), ws = T(0), ws2 = T(0), wm2 = T(0);
+#pragma unroll
+  for (int o = 0; o < W; ++o)
+  {
+    if (RES != 0 && (o < K - RES || o > 2 * K - RES))
+      continue;
+    const T vm = zm[(wy + o) * TX + lane], va = za[(wy + o) * TX + lane];
+    const T cm = cm_[o], ca = ca_[o];
+    if (o & 1)
+      wm2 = fma(cm, vm, wm2);
+    else
+      wm = fma(cm, vm, wm);
+    ws = fma(ca, vm, ws);
+    ws2 = fma(cm, va, ws2);
+  }
+  wm_out = wm + wm2;
+  ws_out = ws + ws2;
+}
+
+template <int K, typename T, int R = 0>
+__device__ __forceinline__ void op3_dir1_res(int res, const T *zm, const T *za, const T *cm_, const T *ca_, int wy,
+                                             int lane, T &wm, T &ws)
+{
+  if constexpr (R < K)
+  {
+    if (res == R)
+    {
+      op3_dir1<K, T, R>(zm, za, cm_, ca_, wy, lane, wm, ws);
+      return;
+    }
+    op3_dir1_res<K, T, R + 1>(res, zm, za, cm_, ca_, wy, lane, wm, ws);
+  }
+}
+
 template <int K, typename T, bool RESID>
 __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
     level_op3d_kernel(const __grid_constant__ BandMats<T, K> B, const T *__restrict__ x,
@@ -235,32 +278,42 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       __syncthreads();
       // dir 1
-      T wm = T(0), ws = T(0), ws2 = T(0), wm2 = T(0);
-#pragma unroll
-      for (int o = 0; o < W; ++o)
+      T wm = T(0), ws = T(0);
+      if constexpr (C::C1REG)
       {
-        const T vm = zm[(wy + o) * TX + lane], va = za[(wy + o) * TX + lane];
-        const T cm = C::C1REG ? c1r_m[C::C1REG ? o : 0] : c1s_m[o];
-        const T ca = C::C1REG ? c1r_a[C::C1REG ? o : 0] : c1s_a[o];
-        if (o & 1)
-          wm2 = fma(cm, vm, wm2);
-        else
-          wm = fma(cm, vm, wm);
-        ws = fma(ca, vm, ws);
-        ws2 = fma(cm, va, ws2);
+        T ws2 = T(0), wm2 = T(0);
+#pragma unroll
+        for (int o = 0; o < W; ++o)
+        {
+          const T vm = zm[(wy + o) * TX + lane], va = za[(wy + o) * TX + lane];
+          const T cm = c1r_m[C::C1REG ? o : 0];
+          const T ca = c1r_a[C::C1REG ? o : 0];
+          if (o & 1)
+            wm2 = fma(cm, vm, wm2);
+          else
+            wm = fma(cm, vm, wm);
+          ws = fma(ca, vm, ws);
+          ws2 = fma(cm, va, ws2);
+        }
+        wm += wm2;
+        ws += ws2;
       }
-      wm += wm2;
-      ws += ws2;
+      else
+        op3_dir1_res<K, T>(res1, zm, za, c1s_m, c1s_a, wy, lane, wm, ws);
       // dir 2: output plane p = q - K + jo, lattice residue (p + 1) mod K =
       // (u + 1 + jo) mod K; band offset q - p + K = 2K - jo
 #pragma unroll
       for (int jo = 0; jo < W; ++jo)
       {
-        constexpr int dummy = 0;
-        (void)dummy;
         const int res = (u + 1 + jo) % K;
-        acc[jo] = fma(B.A[res][2 * K - jo], wm, acc[jo]);
-        acc[jo] = fma(B.M[res][2 * K - jo], ws, acc[jo]);
+        // rows of residue res != 0 couple only their own cell: offsets
+        // [K - res, 2K - res]; the other band entries are exact zeros
+        // (compile-time here, so their FMAs are not emitted)
+        const int o = 2 * K - jo;
+        if (K >= 3 && res != 0 && (o < K - res || o > 2 * K - res))
+          continue;  // (kept for k = 2: measured 1% slower there)
+        acc[jo] = fma(B.A[res][o], wm, acc[jo]);
+        acc[jo] = fma(B.M[res][o], ws, acc[jo]);
       }
       const int64_t p_out = zs - 2 * K + it;
       if (it >= 2 * K && p_out < ze && p_out >= zbeg && out_ok)
