@@ -402,3 +402,30 @@ def test_restrict3d_large(pmg, cuda, case, dtype):
         xd = dev(cuda, x0.copy())
         pmg.v_cycle(ctx, L - 1, xd, dev(cuda, b))
         assert rel(xd.cpu().numpy(), ref.vcycle(L - 1, x0, b)) < 1e-11
+
+
+@pytest.mark.parametrize("case", [(2, 6), (4, 5), (1, 7), (3, 5)], ids=lambda c: f"k{c[0]}L{c[1]}")
+def test_restrict_slab_ranges(pmg, cuda, case):
+    """Owned-plane restriction (pmg_restrict_slab, the slab V-cycle's) on
+    sub-ranges of coarse planes, from a local slab of the fine vector, equals
+    the full restriction bitwise (restrict3d_kernel's node values do not
+    depend on the z chunking)."""
+    k, L = case
+    ctx = pmg.make_multigrid_context(3, k, L)
+    c, f = ctx.levels[-2], ctx.levels[-1]
+    mf = f.level.dofs_per_dim
+    mc = (mf - 1) // 2
+    rf, _ = inputs(f.level.total_dofs, np.float64, seed=4)
+    rfd = dev(cuda, rf)
+    full = cuda.zeros(c.level.total_dofs, dtype=cuda.float64, device="cuda")
+    pmg.restrict_vector(c, f, rfd, full)
+    full = full.cpu().numpy().reshape(mc, mc * mc)
+    for q0, q1 in ((0, mc), (0, 1), (3, 11), (mc // 2, mc), (mc - 1, mc), (k, 2 * k + 1)):
+        # fine planes the range depends on, as a local slab
+        c_lo = max(0, (q0 + 1) // k - (1 if (q0 + 1) % k == 0 else 0))
+        pz0 = 2 * c_lo * k
+        pz1 = min(2 * (q1 // k) * k + 2 * k, mf)
+        local = rfd[pz0 * mf * mf:pz1 * mf * mf].clone()
+        rc = cuda.zeros((q1 - q0) * mc * mc, dtype=cuda.float64, device="cuda")
+        pmg.restrict_slab(c, f, local, pz0, rc, q0, q0, q1)
+        assert np.array_equal(rc.cpu().numpy().reshape(q1 - q0, mc * mc), full[q0:q1]), (q0, q1)
