@@ -84,7 +84,9 @@ void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, 
       return;
     }
   }
-  if constexpr (D == 3 && (PMG_K <= PMG_PLANE_KMAX || (PMG_K == 3 && sizeof(T) == 4)))
+  // (f32 k = 3 went to the plane kernel until the pp kernel's staging rewrite:
+  // pp is now 10% faster there, profiles/r01/ab_f32k3_pp_vs_plane.txt)
+  if constexpr (D == 3 && PMG_K <= PMG_PLANE_KMAX)
   {
     if (impl != SMOOTHER_IMPL_LINE && (mode == MODE_FUSED || mode == MODE_BOUNDARY))
     {
