@@ -417,6 +417,141 @@ __global__ void __launch_bounds__(Rest3Cfg<K>::NT)
   }
 }
 
+// ---------------------------------------------------------------------------
+// 2D transfers in one kernel each (the 2D analogues of prolong3d_kernel and
+// one plane of restrict3d_kernel): a CTA stages its block of the input
+// (coarse cells + 1 node, resp. the fine window of its coarse nodes), runs
+// the x pass into shared memory and the y pass straight to the output.
+// Traffic: prolongation x_c once + x_f read/write (vs + 2 x mf mc scratch),
+// restriction r_f once with the window halo (vs + 2 x mc mf scratch).
+// ---------------------------------------------------------------------------
+#ifndef PMG_PROL2_RY
+#define PMG_PROL2_RY 4
+#endif
+template <int K>
+struct Prol2Cfg
+{
+  static constexpr int CX = (32 / (2 * K)) > 0 ? 32 / (2 * K) : 1;
+  static constexpr int CYT = (16 / (2 * K)) > 0 ? 16 / (2 * K) : 1;  // cells per thread row block
+  static constexpr int RY = PMG_PROL2_RY;                              // row blocks per thread
+  static constexpr int CY = CYT * RY;                                  // cells per CTA along y
+  static constexpr int FX = 2 * K * CX, FY = 2 * K * CYT;              // threads: 32 x FY
+  static constexpr int QX = CX * K + 1, QY = CY * K + 1;
+  static constexpr int NT = 32 * FY;
+};
+
+template <int K, typename T, bool ACC>
+__global__ void __launch_bounds__(Prol2Cfg<K>::NT)
+    prolong2d_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ xc, T *__restrict__ xf, int mc,
+                     int nc)
+{
+  pdl_prologue();
+  using C = Prol2Cfg<K>;
+  constexpr int CX = C::CX, CY = C::CY, FX = C::FX, QX = C::QX, QY = C::QY, NT = C::NT;
+  __shared__ T Ps[2 * K + 1][K + 1];
+  __shared__ T Cs[QY][QX];
+  __shared__ T T1[QY][FX];
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int e = tid; e < (2 * K + 1) * (K + 1); e += NT)
+    (&Ps[0][0])[e] = (&P.P[0][0])[e];
+  const int cx0 = blockIdx.x * CX, cy0 = blockIdx.y * CY;
+  for (int e = tid; e < QY * QX; e += NT)
+  {
+    const int iy = e / QX, ix = e - iy * QX;
+    const int qx = cx0 * K + ix, qy = cy0 * K + iy;  // coarse lattice, 0 and mc + 1 on the boundary
+    Cs[iy][ix] = (qx >= 1 && qx <= mc && qy >= 1 && qy <= mc)
+                     ? __ldg(xc + static_cast<int64_t>(qy - 1) * mc + (qx - 1))
+                     : T(0);
+  }
+  __syncthreads();
+  for (int e = tid; e < QY * FX; e += NT)
+  {
+    const int iy = e / FX, fx = e - iy * FX;
+    const int c = fx / (2 * K), r = fx - 2 * K * c + 1;
+    T s = T(0);
+#pragma unroll
+    for (int t = 0; t <= K; ++t)
+      s = fma(Ps[r][t], Cs[iy][c * K + t], s);
+    T1[iy][fx] = s;
+  }
+  __syncthreads();
+  const int fx = threadIdx.x;
+  if (fx >= FX)
+    return;
+  const int cxl = fx / (2 * K), rx = fx - 2 * K * cxl + 1;
+  const int mf = 2 * mc + 1;
+  const int px = 2 * (cx0 + cxl) * K + rx;  // fine lattice
+  if (cx0 + cxl >= nc || px > mf)
+    return;
+#pragma unroll
+  for (int rb = 0; rb < C::RY; ++rb)
+  {
+    const int fy = threadIdx.y + rb * C::FY;
+    const int cyl = fy / (2 * K), ry = fy - 2 * K * cyl + 1;
+    const int py = 2 * (cy0 + cyl) * K + ry;
+    if (cy0 + cyl >= nc || py > mf)
+      break;
+    T s = T(0);
+#pragma unroll
+    for (int t = 0; t <= K; ++t)
+      s = fma(Ps[ry][t], T1[cyl * K + t][fx], s);
+    T *o = xf + static_cast<int64_t>(py - 1) * mf + (px - 1);
+    if constexpr (ACC)
+      *o += s;
+    else
+      *o = s;
+  }
+}
+
+template <int K>
+struct Rest2Cfg
+{
+  static constexpr int CX = 32 / K, CY = (16 / K) >= 2 ? 16 / K : 2;
+  static constexpr int OX = CX * K, OY = CY * K;
+  static constexpr int WX = 2 * K * (CX + 1), WY = 2 * K * (CY + 1), WN = WX * WY;
+  static constexpr int NT = 32 * OY;
+};
+
+template <int K, typename T>
+__global__ void __launch_bounds__(Rest2Cfg<K>::NT)
+    restrict2d_kernel(const __grid_constant__ ProlMats<T, K> P, const T *__restrict__ rf, T *__restrict__ rc,
+                      T *__restrict__ zero, int mc)
+{
+  using C = Rest2Cfg<K>;
+  constexpr int CX = C::CX, CY = C::CY, OX = C::OX, OY = C::OY, WX = C::WX, WY = C::WY, NT = C::NT;
+  __shared__ T Ps[2 * K + 1][K + 1];
+  __shared__ __align__(16) T F[WY * WX];
+  __shared__ T R1[WY][OX];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  for (int e = tid; e < (2 * K + 1) * (K + 1); e += NT)
+    (&Ps[0][0])[e] = (&P.P[0][0])[e];
+  const int mf = 2 * mc + 1;
+  const int cx0 = blockIdx.x * CX, cy0 = blockIdx.y * CY;
+  const int fx0 = 2 * cx0 * K, fy0 = 2 * cy0 * K;  // 0-based fine index of window (0, 0)
+  pdl_prologue();
+  for (int e = tid; e < C::WN; e += NT)
+  {
+    const int fy = e / WX, fx = e - fy * WX;
+    const bool ok = fy0 + fy < mf && fx0 + fx < mf;
+    tr_cp_async(&F[e], ok ? rf + static_cast<int64_t>(fy0 + fy) * mf + (fx0 + fx) : rf, ok);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  const int qx = cx0 * K + 1 + tx, qy = cy0 * K + 1 + ty;
+  if (tx < OX)
+    for (int fy = ty; fy < WY; fy += OY)
+      R1[fy][tx] = rest_gather_1d<K, T>(Ps, qx, cx0, [&](int o) { return F[fy * WX + o]; });
+  __syncthreads();
+  if (tx >= OX || qx > mc || qy > mc)
+    return;
+  const T v = rest_gather_1d<K, T>(Ps, qy, cy0, [&](int o) { return R1[o][tx]; });
+  const int64_t idx = static_cast<int64_t>(qy - 1) * mc + (qx - 1);
+  rc[idx] = v;
+  if (zero)
+    zero[idx] = T(0);
+}
+
 template <int D, int K, typename T>
 void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, int64_t mc,
                        T *tA, T *tB, int sm_count, cudaStream_t s)
@@ -424,6 +559,18 @@ void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, in
   const int64_t mf = 2 * mc + 1;
   if constexpr (D == 2)
   {
+    if (use_fused_transfer())
+    {
+      using C = Prol2Cfg<K>;
+      const int nc = static_cast<int>((mc + 1) / K);
+      const dim3 grid((nc + C::CX - 1) / C::CX, (nc + C::CY - 1) / C::CY);
+      if (acc)
+        pdl_launch(prolong2d_kernel<K, T, true>, grid, dim3(32, C::FY), 0, s, P, xc, xf, static_cast<int>(mc), nc);
+      else
+        pdl_launch(prolong2d_kernel<K, T, false>, grid, dim3(32, C::FY), 0, s, P, xc, xf, static_cast<int>(mc), nc);
+      check_launch("prolong2d_kernel");
+      return;
+    }
     pdl_launch(prolong_pass_kernel<K, T, 0, false>, pass_grid(mf, mc, 1), dim3(32, 8), 0, s, P, xc, tA, mf, mc, 1, mc, int64_t(0));
     check_launch("prolong_pass0");
     if (acc)
@@ -496,6 +643,14 @@ void launch_restrict(const ProlMats<T, K> &P, const T *rf, T *rc, T *zero, int64
   const int64_t mf = 2 * mc + 1;
   if constexpr (D == 2)
   {
+    if (use_fused_transfer())
+    {
+      using C = Rest2Cfg<K>;
+      const dim3 grid(static_cast<unsigned>((mc + C::OX - 1) / C::OX), static_cast<unsigned>((mc + C::OY - 1) / C::OY));
+      pdl_launch(restrict2d_kernel<K, T>, grid, dim3(32, C::OY), 0, s, P, rf, rc, zero, static_cast<int>(mc));
+      check_launch("restrict2d_kernel");
+      return;
+    }
     pdl_launch(restrict_pass_kernel<K, T, 0>, pass_grid(mc, mf, 1), dim3(32, 8), 0, s, P, rf, tA, mc, mf, 1, mf, int64_t(0),
                static_cast<T *>(nullptr));
     check_launch("restrict_pass0");

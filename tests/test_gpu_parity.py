@@ -429,3 +429,23 @@ def test_restrict_slab_ranges(pmg, cuda, case):
         rc = cuda.zeros((q1 - q0) * mc * mc, dtype=cuda.float64, device="cuda")
         pmg.restrict_slab(c, f, local, pz0, rc, q0, q0, q1)
         assert np.array_equal(rc.cpu().numpy().reshape(q1 - q0, mc * mc), full[q0:q1]), (q0, q1)
+
+
+# prolong2d_kernel / restrict2d_kernel on levels with many tiles
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", [(2, 1, 9), (2, 2, 8), (2, 3, 7), (2, 5, 6), (2, 7, 6)],
+                         ids=lambda c: f"d{c[0]}k{c[1]}L{c[2]}")
+def test_transfers2d_large(pmg, cuda, case, dtype):
+    dim, k, L = case
+    ref = refbind.RefMg(dim, k, L, prec=0 if dtype == np.float64 else 1)
+    ctx = pmg.make_multigrid_context(dim, k, L, dtype=dtype)
+    c, f = ctx.levels[-2], ctx.levels[-1]
+    tdt = cuda.float64 if dtype == np.float64 else cuda.float32
+    xc, _ = inputs(c.level.total_dofs, dtype, seed=7)
+    rf, _ = inputs(f.level.total_dofs, dtype, seed=9)
+    base = dev(cuda, rf.copy())
+    pmg.prolongate(c, f, dev(cuda, xc), base, accumulate=True)
+    assert rel(base.cpu().numpy(), rf.astype(np.float64) + ref.prolongate(L - 2, xc)) < TOL[dtype]
+    rc = cuda.zeros(c.level.total_dofs, dtype=tdt, device="cuda")
+    pmg.restrict_vector(c, f, dev(cuda, rf), rc)
+    assert rel(rc.cpu().numpy(), ref.restrict(L - 2, rf)) < TOL[dtype]
