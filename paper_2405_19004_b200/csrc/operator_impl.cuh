@@ -20,6 +20,7 @@
 // Band coefficients depend only on the lattice residue p mod k.
 #pragma once
 
+
 #include "common.cuh"
 
 namespace pmgb
@@ -332,107 +333,134 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
   }
 }
 
+// 2D: CTA = 128 columns marching down a chunk of rows that starts on a
+// multiple of K (so every row's lattice residue, and with it the dir-1 band
+// row, is a compile-time constant of the K-fold unrolled row loop: the
+// structurally zero taps are dropped and the coefficients are parameter-bank
+// operands), a 3-deep cp.async row ring (one barrier per row) and a register
+// shift ring of the 2K+1 rows in flight — the 3D kernel's organisation.
 template <int K, typename T, bool RESID>
 __global__ void __launch_bounds__(128)
     level_op2d_kernel(const __grid_constant__ BandMats<T, K> B, const T *__restrict__ x,
-                      const T *__restrict__ b, T *__restrict__ y, int64_t m, int rchunk)
+                         const T *__restrict__ b, T *__restrict__ y, int64_t m, int rchunk)
 {
   pdl_prologue();
-  constexpr int T0 = 128, W = 2 * K + 1, R = 2 * K + 1, XW = T0 + 2 * K;
-  __shared__ __align__(16) T Xs[2][XW];
-  __shared__ T bm[K][W], ba[K][W];
-  const int tid = threadIdx.x;
-  for (int e = tid; e < K * W; e += T0)
-  {
-    (&bm[0][0])[e] = (&B.M[0][0])[e];
-    (&ba[0][0])[e] = (&B.A[0][0])[e];
-  }
+  constexpr int T0 = 128, W = 2 * K + 1, XW = T0 + 2 * K;
+  constexpr int NL = (XW + T0 - 1) / T0;
+  __shared__ __align__(16) T Xs[3][XW];
+  const int i = threadIdx.x;
   const int64_t g0 = static_cast<int64_t>(blockIdx.x) * T0;
-  const int64_t rs = static_cast<int64_t>(blockIdx.y) * rchunk;
+  const int64_t rs = static_cast<int64_t>(blockIdx.y) * rchunk;  // multiple of K
   const int64_t re = min(rs + rchunk, m);
-  const int i = tid;
-  __syncthreads();
   T c0m[W], c0a[W];
   {
     const int res0 = static_cast<int>((g0 + i + 1) % K);
 #pragma unroll
     for (int o = 0; o < W; ++o)
     {
-      c0m[o] = bm[res0][o];
-      c0a[o] = ba[res0][o];
+      c0m[o] = B.M[res0][o];
+      c0a[o] = B.A[res0][o];
     }
   }
-  auto load_row = [&](int64_t q, int buf) {
+  int off[NL];
+  bool okx[NL];
+#pragma unroll
+  for (int j = 0; j < NL; ++j)
+  {
+    const int e = i + j * T0;
+    const int64_t gx = g0 - K + e;
+    okx[j] = e < XW && gx >= 0 && gx < m;
+    off[j] = okx[j] ? static_cast<int>(gx) : 0;
+  }
+  const bool col_ok = g0 + i < m;
+  const int NPL = static_cast<int>(re - rs) + 2 * K;  // input rows rs-K .. re+K-1
+  auto issue = [&](int it) {
+    const int64_t q = rs - K + it;
     const bool rin = q >= 0 && q < m;
-    for (int e = tid; e < XW; e += T0)
+    const T *xr = x + (rin ? q : 0) * m;
+    T *dst = Xs[it % 3];
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
     {
-      const int64_t gx = g0 - K + e;
-      const bool ok = rin && gx >= 0 && gx < m;
-      op_cp_async(&Xs[buf][e], ok ? x + q * m + gx : x, ok);
+      const int e = i + j * T0;
+      if (e < XW)
+        op_cp_async(dst + e, xr + off[j], rin && okx[j]);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
-  const int NPL = static_cast<int>(re - rs) + 2 * K;
-  T acc[R];
+  T acc[W];
 #pragma unroll
-  for (int o = 0; o < R; ++o)
+  for (int o = 0; o < W; ++o)
     acc[o] = T(0);
-  load_row(rs - K, 0);
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  issue(0);
+  if (NPL > 1)
+  {
+    issue(1);
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  }
+  else
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
-  for (int base = 0; base < NPL; base += R)
+  for (int base = 0; base < NPL; base += K)
   {
 #pragma unroll
-    for (int u = 0; u < R; ++u)
+    for (int u = 0; u < K; ++u)
     {
-      const int it = base + u;
-      if (it < NPL)
+      const int it = base + u;  // uniform across the CTA
+      if (it >= NPL)
+        break;
+      if (it + 2 < NPL)
+        issue(it + 2);
+      const T *xs = Xs[it % 3] + i;
+      T zm0 = c0m[0] * xs[0], za0 = c0a[0] * xs[0], zm1 = c0m[1] * xs[1], za1 = c0a[1] * xs[1];
+#pragma unroll
+      for (int o = 2; o < W; o += 2)
       {
-        const int buf = it & 1;
-        const int64_t q = rs - K + it;
-        if (it + 1 < NPL)
-          load_row(q + 1, buf ^ 1);
-        const int64_t p_out = q - K;
-        const bool emit = it >= 2 * K && p_out < re && g0 + i < m;
-        T bval = T(0);
-        if constexpr (RESID)
+        zm0 = fma(c0m[o], xs[o], zm0);
+        za0 = fma(c0a[o], xs[o], za0);
+        if (o + 1 < W)
         {
-          if (emit)
-            bval = __ldg(b + p_out * m + g0 + i);
+          zm1 = fma(c0m[o + 1], xs[o + 1], zm1);
+          za1 = fma(c0a[o + 1], xs[o + 1], za1);
         }
-        T zm = T(0), za = T(0);
-#pragma unroll
-        for (int o = 0; o < W; ++o)
-        {
-          zm = fma(c0m[o], Xs[buf][i + o], zm);
-          za = fma(c0a[o], Xs[buf][i + o], za);
-        }
-        // 2D: y = A1 zM + M1 zA along direction 1
-        const int rq = static_cast<int>(((q + 1) % K + K) % K);
-#pragma unroll
-        for (int oo = 0; oo < W; ++oo)
-        {
-          int res = rq + (oo % K);
-          if (res >= K)
-            res -= K;
-          const int slot = ((u - K + oo) % R + R) % R;
-          acc[slot] = fma(ba[res][2 * K - oo], zm, acc[slot]);
-          acc[slot] = fma(bm[res][2 * K - oo], za, acc[slot]);
-        }
-        const int sl_out = ((u - K) % R + R) % R;
-        if (emit)
-        {
-          const int64_t idx = p_out * m + g0 + i;
-          if constexpr (RESID)
-            y[idx] = bval - acc[sl_out];
-          else
-            y[idx] = acc[sl_out];
-        }
-        acc[sl_out] = T(0);
-        if (it + 1 < NPL)
-          asm volatile("cp.async.wait_all;\n" ::: "memory");
-        __syncthreads();
       }
+      const T zm = zm0 + zm1, za = za0 + za1;
+      const int64_t p_out = rs - 2 * K + it;
+      T bval = T(0);
+      if constexpr (RESID)
+      {
+        if (it >= 2 * K && p_out < re && col_ok)
+          bval = __ldg(b + p_out * m + g0 + i);
+      }
+      if (it + 2 < NPL)
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
+      // dir 1: output row p = q - K + jo has lattice residue (u + 1 + jo) mod K
+      // and band offset 2K - jo; rows of residue != 0 couple only their cell
+#pragma unroll
+      for (int jo = 0; jo < W; ++jo)
+      {
+        const int res = (u + 1 + jo) % K;
+        const int o = 2 * K - jo;
+        if (res != 0 && (o < K - res || o > 2 * K - res))
+          continue;
+        acc[jo] = fma(B.A[res][o], zm, acc[jo]);
+        acc[jo] = fma(B.M[res][o], za, acc[jo]);
+      }
+      if (it >= 2 * K && p_out < re && col_ok)
+      {
+        const int64_t idx = p_out * m + g0 + i;
+        if constexpr (RESID)
+          y[idx] = bval - acc[0];
+        else
+          y[idx] = acc[0];
+      }
+#pragma unroll
+      for (int jo = 0; jo < W - 1; ++jo)
+        acc[jo] = acc[jo + 1];
+      acc[W - 1] = T(0);
     }
   }
 }
@@ -480,6 +508,7 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
     int64_t ny = (want + gx - 1) / gx;
     int64_t rchunk = (m + ny - 1) / ny;
     rchunk = std::max<int64_t>(rchunk, std::min<int64_t>(m, 4 * K));
+    rchunk = ((rchunk + K - 1) / K) * K;  // chunks start on multiples of K
     const unsigned gy = static_cast<unsigned>((m + rchunk - 1) / rchunk);
     auto kern = b ? level_op2d_kernel<K, T, true> : level_op2d_kernel<K, T, false>;
     pdl_launch(kern, dim3(gx, gy), 128, 0, s, B, x, b, y, m, static_cast<int>(rchunk));
