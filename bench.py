@@ -191,7 +191,7 @@ def smoother_kernel_name(args):
         return "vp_patch3d_kernel" if per_colour >= 65536 else "vp_smooth_plane_kernel"
     if args.dim == 2 and (args.degree in (2, 3) or (args.degree == 4 and args.dtype == "f32")):
         return "vp_patch2d_kernel"
-    if args.dim == 3 and (args.degree in (3, 4) or (args.degree == 5 and args.dtype == "f32")):
+    if args.dim == 3 and (args.degree in (3, 4) or (args.degree in (5, 6) and args.dtype == "f32")):
         return "vp_smooth_pp_kernel"
     return "vp_smooth_kernel"
 

@@ -97,7 +97,8 @@ void smooth_entry(const void *P, const ColorArgs<T> &a, int mode, int sm_count, 
       return;
     }
   }
-  if constexpr (D == 3 && (PMG_K == 3 || PMG_K == 4 || (PMG_K == 5 && sizeof(T) == 4)))
+  // f32 k = 6 too (profiles/r01/ab_pp_f32_k67.txt: +5-11%; k = 7 f32 -4%)
+  if constexpr (D == 3 && (PMG_K == 3 || PMG_K == 4 || ((PMG_K == 5 || PMG_K == 6) && sizeof(T) == 4)))
   {
     // degree 3, 4 (and 5 in f32): ping-pong layouts (smoother_pp.cuh) unless
     // the in-place line kernel is selected. Measured (profiles/r01): +6..11%
