@@ -14,6 +14,7 @@
 // prolongation pass can accumulate into x (the V-cycle's x += P x_c).
 #pragma once
 
+
 #include <cstdlib>
 
 #include "common.cuh"
@@ -233,23 +234,54 @@ __global__ void __launch_bounds__(Prol3Cfg<K>::NT)
     return;
   const int64_t mf2 = static_cast<int64_t>(mf) * mf;
   T *o = xf + static_cast<int64_t>(py - 1) * mf + (px - 1);
-#pragma unroll
-  for (int rz = 1; rz <= 2 * K; ++rz)
+  if constexpr (K <= 4)
   {
-    const int pz = 2 * cz * K + rz;
-    if (pz > mf || pz - 1 >= f1)
-      break;
-    if (pz - 1 < f0)  // fine planes [f0, f1) only (0-based)
-      continue;
-    T s = T(0);
+    // all 2K accumulated outputs of the column: issue every load of x_f before
+    // the first store, so the read latencies overlap instead of serialising
+    // the read-modify-write chain (profiles/r01/ab_prolong3d_batch.txt: k = 1,
+    // 2 and f32 -14..18%, k = 3 -7%; for k >= 5 the 2K live values cost more)
+    T old[2 * K];
+    bool okz[2 * K];
 #pragma unroll
-    for (int t = 0; t <= K; ++t)
-      s = fma(Ps[rz][t], T2[t][fy][fx], s);
-    T *op = o + (pz - 1) * mf2;
-    if constexpr (ACC)
-      *op += s;
-    else
-      *op = s;
+    for (int rz = 1; rz <= 2 * K; ++rz)
+    {
+      const int pz = 2 * cz * K + rz;
+      okz[rz - 1] = pz <= mf && pz - 1 >= f0 && pz - 1 < f1;  // fine planes [f0, f1) only (0-based)
+      if constexpr (ACC)
+        old[rz - 1] = okz[rz - 1] ? o[(pz - 1) * mf2] : T(0);
+    }
+#pragma unroll
+    for (int rz = 1; rz <= 2 * K; ++rz)
+    {
+      if (!okz[rz - 1])
+        continue;
+      T v = T(0);
+#pragma unroll
+      for (int t = 0; t <= K; ++t)
+        v = fma(Ps[rz][t], T2[t][fy][fx], v);
+      o[(2 * cz * K + rz - 1) * mf2] = ACC ? old[rz - 1] + v : v;
+    }
+  }
+  else
+  {
+#pragma unroll
+    for (int rz = 1; rz <= 2 * K; ++rz)
+    {
+      const int pz = 2 * cz * K + rz;
+      if (pz > mf || pz - 1 >= f1)
+        break;
+      if (pz - 1 < f0)  // fine planes [f0, f1) only (0-based)
+        continue;
+      T s = T(0);
+#pragma unroll
+      for (int t = 0; t <= K; ++t)
+        s = fma(Ps[rz][t], T2[t][fy][fx], s);
+      T *op = o + (pz - 1) * mf2;
+      if constexpr (ACC)
+        *op += s;
+      else
+        *op = s;
+    }
   }
 }
 
