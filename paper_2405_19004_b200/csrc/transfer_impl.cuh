@@ -515,23 +515,33 @@ __global__ void __launch_bounds__(Prol2Cfg<K>::NT)
   const int px = 2 * (cx0 + cxl) * K + rx;  // fine lattice
   if (cx0 + cxl >= nc || px > mf)
     return;
+  // the RY accumulated outputs: all loads of x_f before the first store
+  T old[C::RY];
+  bool ok[C::RY];
+  T *o[C::RY];
 #pragma unroll
   for (int rb = 0; rb < C::RY; ++rb)
   {
     const int fy = threadIdx.y + rb * C::FY;
     const int cyl = fy / (2 * K), ry = fy - 2 * K * cyl + 1;
     const int py = 2 * (cy0 + cyl) * K + ry;
-    if (cy0 + cyl >= nc || py > mf)
-      break;
+    ok[rb] = cy0 + cyl < nc && py <= mf;
+    o[rb] = xf + static_cast<int64_t>(ok[rb] ? py - 1 : 0) * mf + (px - 1);
+    if constexpr (ACC)
+      old[rb] = ok[rb] ? *o[rb] : T(0);
+  }
+#pragma unroll
+  for (int rb = 0; rb < C::RY; ++rb)
+  {
+    if (!ok[rb])
+      continue;
+    const int fy = threadIdx.y + rb * C::FY;
+    const int cyl = fy / (2 * K), ry = fy - 2 * K * cyl + 1;
     T s = T(0);
 #pragma unroll
     for (int t = 0; t <= K; ++t)
       s = fma(Ps[ry][t], T1[cyl * K + t][fx], s);
-    T *o = xf + static_cast<int64_t>(py - 1) * mf + (px - 1);
-    if constexpr (ACC)
-      *o += s;
-    else
-      *o = s;
+    *o[rb] = ACC ? old[rb] + s : s;
   }
 }
 
