@@ -21,6 +21,7 @@
 #pragma once
 
 
+
 #include "common.cuh"
 
 namespace pmgb
@@ -352,9 +353,23 @@ __global__ void __launch_bounds__(128)
   const int64_t g0 = static_cast<int64_t>(blockIdx.x) * T0;
   const int64_t rs = static_cast<int64_t>(blockIdx.y) * rchunk;  // multiple of K
   const int64_t re = min(rs + rchunk, m);
-  T c0m[W], c0a[W];
+  // dir-0 band row of this lane's residue: in registers, or for K = 4, 5 read
+  // from shared memory (2 (2K+1) registers fewer -> more resident CTAs;
+  // profiles/r01/ab_levelop2d_coef_smem.txt: k = 4 -14%, k = 5 -4%; k = 7 +6%)
+  constexpr bool C0S = K == 4 || K == 5;
+  __shared__ T c0s[C0S ? 2 : 1][C0S ? K : 1][C0S ? W : 1];
+  T c0m[C0S ? 1 : W], c0a[C0S ? 1 : W];
+  const int res0 = static_cast<int>((g0 + i + 1) % K);
+  if constexpr (C0S)
   {
-    const int res0 = static_cast<int>((g0 + i + 1) % K);
+    for (int e = i; e < K * W; e += T0)
+    {
+      c0s[0][e / W][e % W] = (&B.M[0][0])[e];
+      c0s[1][e / W][e % W] = (&B.A[0][0])[e];
+    }
+  }
+  else
+  {
 #pragma unroll
     for (int o = 0; o < W; ++o)
     {
@@ -362,6 +377,18 @@ __global__ void __launch_bounds__(128)
       c0a[o] = B.A[res0][o];
     }
   }
+  auto cm0 = [&](int o) -> T {
+    if constexpr (C0S)
+      return c0s[0][res0][o];
+    else
+      return c0m[o];
+  };
+  auto ca0 = [&](int o) -> T {
+    if constexpr (C0S)
+      return c0s[1][res0][o];
+    else
+      return c0a[o];
+  };
   int off[NL];
   bool okx[NL];
 #pragma unroll
@@ -412,16 +439,16 @@ __global__ void __launch_bounds__(128)
       if (it + 2 < NPL)
         issue(it + 2);
       const T *xs = Xs[it % 3] + i;
-      T zm0 = c0m[0] * xs[0], za0 = c0a[0] * xs[0], zm1 = c0m[1] * xs[1], za1 = c0a[1] * xs[1];
+      T zm0 = cm0(0) * xs[0], za0 = ca0(0) * xs[0], zm1 = cm0(1) * xs[1], za1 = ca0(1) * xs[1];
 #pragma unroll
       for (int o = 2; o < W; o += 2)
       {
-        zm0 = fma(c0m[o], xs[o], zm0);
-        za0 = fma(c0a[o], xs[o], za0);
+        zm0 = fma(cm0(o), xs[o], zm0);
+        za0 = fma(ca0(o), xs[o], za0);
         if (o + 1 < W)
         {
-          zm1 = fma(c0m[o + 1], xs[o + 1], zm1);
-          za1 = fma(c0a[o + 1], xs[o + 1], za1);
+          zm1 = fma(cm0(o + 1), xs[o + 1], zm1);
+          za1 = fma(ca0(o + 1), xs[o + 1], za1);
         }
       }
       const T zm = zm0 + zm1, za = za0 + za1;
