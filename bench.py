@@ -209,6 +209,94 @@ def config_dict(args):
             "l2_flush": "256 MiB write before every timed step"}
 
 
+# C3 (3D, ~1e8 DoF) and C4 (2D, ~2e8 DoF) finest levels per degree
+C3_LEVELS = {1: 9, 2: 8, 3: 7, 4: 7, 5: 6, 6: 6, 7: 6}
+C4_LEVELS = {1: 14, 2: 13, 3: 12, 4: 12, 5: 11, 6: 11, 7: 11}
+
+
+def time_smoother(pmg, torch, lev, x, b, variant, steps, warmup, flush, stream):
+    """Mean device time (s) of one smoothing step: W untimed steps, then K
+    steps each bracketed by CUDA events with an L2 flush before each."""
+    for _ in range(warmup):
+        pmg.smooth(lev, x, b, variant)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(float(i))
+        ev[i][0].record(stream)
+        pmg.smooth(lev, x, b, variant)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(c) for a, c in ev) / 1e3 / steps
+
+
+def sweep_entry(pmg, torch, dim, k, L, dtype, variant, steps, flush, stream, hbm_peak, max_mhz, sm_count,
+                vcycle=False):
+    """One configuration of a degree sweep: smoother step (and optionally one
+    graph-captured V-cycle) with the same timing rules as the headline."""
+    np_dt = np.float64 if dtype == "f64" else np.float32
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    word = 8 if dtype == "f64" else 4
+    ctx = pmg.make_multigrid_context(dim, k, L, variant, dtype=np_dt)
+    lev = ctx.levels[-1]
+    N = lev.level.total_dofs
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.rand(N, dtype=tdt, device="cuda", generator=gen) * 2 - 1
+    b = torch.rand(N, dtype=tdt, device="cuda", generator=gen) * 2 - 1
+    t = time_smoother(pmg, torch, lev, x, b, variant, steps, 2, flush, stream)
+    P = ((1 << L) - 1) ** dim
+    flops = flops_per_patch(dim, k) * P
+    byts = algorithmic_bytes_per_step(dim, k, L, word)
+    fp_peak = sm_count * (64 if dtype == "f64" else 128) * 2 * max_mhz * 1e6
+    e = {"dim": dim, "degree": k, "level": L, "dtype": dtype, "variant": variant, "dofs": N,
+         "kernel": pmg.smoother_kernel(lev, variant, 0), "value": N / t, "unit": "DoF/s",
+         "ms_per_step": t * 1e3, "fp_frac": flops / t / fp_peak, "hbm_frac": byts / t / (hbm_peak * 1e9)}
+    if vcycle:
+        li = L - 1
+        pmg.v_cycle(ctx, li, x, b, use_graph=True)
+        torch.cuda.synchronize()
+        vt = 0.0
+        for _ in range(3):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pmg.v_cycle(ctx, li, x, b, use_graph=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            vt += e0.elapsed_time(e1) / 1e3 / 3
+        e["vcycle_value"] = N / vt
+        e["vcycle_ms"] = vt * 1e3
+    del x, b, ctx, lev
+    torch.cuda.empty_cache()
+    return e
+
+
+def run_sweeps(args, pmg, torch, flush, stream, hbm_peak, max_mhz, sm_count):
+    """C3 (3D Q1..Q7 ~1e8 DoF, f64 and f32, smoother step + V-cycle) and the
+    "fused vs straightforward" comparison (BASELINE configs[3]: 2D Q1..Q7
+    ~2e8 DoF; plus 3D Q2 / Q4): naive = the reference's per-patch body moved
+    to the GPU directly (csrc/naive.cu, one CTA per patch, global-memory
+    scratch)."""
+    K = args.sweep_steps
+    common = (K, flush, stream, hbm_peak, max_mhz, sm_count)
+    sweep = []
+    for dtype in ("f64", "f32"):
+        for k in range(1, 8):
+            sweep.append(sweep_entry(pmg, torch, 3, k, C3_LEVELS[k], dtype, "fused", *common, vcycle=True))
+    comp = []
+    cases = [(2, k, C4_LEVELS[k]) for k in range(1, 8)] + [(3, 2, 8), (3, 4, 7)]
+    for dim, k, L in cases:
+        fused = next((e for e in sweep if e["dim"] == dim and e["degree"] == k and e["level"] == L
+                      and e["dtype"] == "f64"), None)
+        if fused is None:
+            fused = sweep_entry(pmg, torch, dim, k, L, "f64", "fused", *common)
+        naive = sweep_entry(pmg, torch, dim, k, L, "f64", "naive", 2, *common[1:])
+        comp.append({"dim": dim, "degree": k, "level": L, "dofs": fused["dofs"], "dtype": "f64",
+                     "fused": fused["value"], "fused_kernel": fused["kernel"], "naive": naive["value"],
+                     "speedup": fused["value"] / naive["value"], "unit": "DoF/s"})
+    return comp, sweep
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -222,6 +310,8 @@ def main():
     ap.add_argument("--variant", default="fused")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU reference work (cpu_baseline)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C3/C4 degree sweeps and the naive comparator")
+    ap.add_argument("--sweep-steps", type=int, default=5)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -272,9 +362,6 @@ def main():
             pmg.smooth(lev, x, b, args.variant)
 
         colour_patch_counts = [colour_patches(args.dim, args.level, c) for c in range(1 << args.dim)]
-
-        def colour_launch(c):
-            pmg.smooth_color(lev, c, x, b, args.variant)
     else:
         # weak scaling: a stack of `world` unit cubes along z, one slab per
         # rank, per-colour halo planes over NCCL overlapped with the interior
@@ -299,9 +386,6 @@ def main():
             for ax in range(2):
                 cnt *= n // 2 if (c >> ax) & 1 else n // 2 - 1
             colour_patch_counts.append(cnt)
-
-        def colour_launch(c):
-            pmg.smooth_color_slab(lev, c, x, b, plan.lo, plan.nz, plan.a, plan.b, args.variant)
 
     def barrier():
         torch.cuda.synchronize()
@@ -377,23 +461,15 @@ def main():
         t_step = float(t.item())
     value = N_total / t_step
 
-    # ---- per-launch roofline of the dominant kernel (the per-colour smoother) --
+    # ---- roofline of the dominant kernel, from the TIMED steps -----------------
+    # A step is exactly the 2^d colour launches of the smoother kernel and
+    # nothing else (profiles/r02: ncu launch list of this command), so the
+    # kernel's average launch duration is ms_per_step / launches per step and
+    # its algorithmic bytes / flops per launch are the step's / launches per
+    # step: achieved = algorithmic per step / t_step (no re-timed warm-L2 launches).
     F = flops_per_patch(args.dim, args.degree)
-    colour_ms, colour_flops = 0.0, 0.0
-    reps = max(3, min(20, args.steps))
-    for c in range(1 << args.dim):
-        if colour_patch_counts[c] == 0:
-            continue
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        flush.fill_(0.5)
-        e0.record(stream)
-        for _ in range(reps):
-            colour_launch(c)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        colour_ms += e0.elapsed_time(e1) / reps
-        colour_flops += F * colour_patch_counts[c]
-    launch_s = colour_ms / 1e3
+    step_flops = float(F * sum(colour_patch_counts))
+    launches_per_step = sum(1 for c in colour_patch_counts if c)
     if world == 1:
         alg_bytes = algorithmic_bytes_per_step(args.dim, args.degree, args.level, word)
     else:  # this rank's slab: x read per colour + b^I read / x^I written per patch
@@ -404,31 +480,40 @@ def main():
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     max_mhz = peaks.get("sm_max_mhz", 1965.0)
     fp_peak = sm_count * (64 if args.dtype == "f64" else 128) * 2 * max_mhz * 1e6 / 1e12
-    traffic = None
+    traffic, traffic_note = None, None
     if os.path.exists(NCU_SUMMARY):
         try:
             s = json.load(open(NCU_SUMMARY))
             key = f"d{args.dim}k{args.degree}L{args.level}{args.dtype}{args.variant}"
-            per = s.get(key, {}).get("dram_bytes_per_launch")
-            if per:  # ncu captured colour launch(es), cold L2: scale to the 2^d launches of a step
-                traffic = float(np.mean(per)) * sum(1 for c in colour_patch_counts if c)
+            ent = s.get(key, {})
+            if ent.get("dram_bytes_per_step"):
+                traffic = float(ent["dram_bytes_per_step"]) / launches_per_step
+                traffic_note = ent.get("note")
         except Exception:
             traffic = None
+    kname = pmg.smoother_kernel(lev, args.variant, 0)
     roofline = {
-        "bound": "hbm", "achieved": alg_bytes / launch_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
-        "frac": alg_bytes / launch_s / 1e9 / hbm_peak, "traffic": traffic,
-        "traffic_note": "DRAM read+write bytes per step from ncu --set full (profiles/ncu_summary.json; "
-                        "cold L2, per-colour launch x colours)",
-        "kernel": smoother_kernel_name(args) + " (one launch per colour, summed over the 2^d colours)",
+        "bound": "hbm", "achieved": alg_bytes / t_step / 1e9, "peak": hbm_peak, "unit": "GB/s",
+        "frac": alg_bytes / t_step / 1e9 / hbm_peak, "traffic": traffic,
+        "traffic_note": traffic_note or "no ncu capture for this configuration",
+        "kernel": kname + f" ({launches_per_step} launches per step = the whole step)",
+        "algorithmic_bytes_per_launch": alg_bytes / launches_per_step,
+        "launch_ms": t_step * 1e3 / launches_per_step,
         "algorithmic_bytes_per_step": alg_bytes,
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
     }
     roofline_fp = {
-        "bound": f"{args.dtype} CUDA-core FMA", "achieved": colour_flops / launch_s / 1e12,
-        "peak": fp_peak, "unit": "TFLOP/s", "frac": colour_flops / launch_s / 1e12 / fp_peak,
-        "algorithmic_flops_per_patch": F,
+        "bound": f"{args.dtype} CUDA-core FMA", "achieved": step_flops / t_step / 1e12,
+        "peak": fp_peak, "unit": "TFLOP/s", "frac": step_flops / t_step / 1e12 / fp_peak,
+        "algorithmic_flops_per_patch": F, "algorithmic_flops_per_launch": step_flops / launches_per_step,
         "peak_source": f"{sm_count} SMs x {64 if args.dtype == 'f64' else 128} FMA/clk x 2 x {max_mhz} MHz",
     }
+    # which roofline binds: at sizes whose x and b fit in L2 (C2: 2 x 16 MiB of
+    # 126 MB) only the first colour of a step reads HBM, so the FP pipe (and
+    # the issue rate) is the limit, not HBM
+    fits_l2 = 2 * N_total * word < 100e6
+    ridge = fp_peak * 1e12 / (hbm_peak * 1e9)  # flop/B
+    binding = "roofline" if (not fits_l2 and step_flops / alg_bytes < ridge) else "roofline_fp"
 
     # on-chip (shared-memory) roofline of the reference's contraction sequence
     # (banksim.py, the paper's model) for the same flops
@@ -513,7 +598,8 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic (x, b ~ U(-1,1))", "config": cfg,
-        "roofline": roofline, "roofline_fp": roofline_fp, "roofline_onchip": roofline_onchip,
+        "roofline": roofline, "roofline_fp": roofline_fp, "roofline_binding": binding,
+        "roofline_onchip": roofline_onchip,
         "e2e": {"value": N_total / t_e2e, "unit": "DoF/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "api": "pmg_smooth_host (C-ABI, pinned host buffers)" if world == 1 else
@@ -522,6 +608,11 @@ def main():
     }
     if vcycle is not None:
         out["vcycle"] = vcycle
+    if world == 1 and not args.no_sweep:
+        del x, b, xh, bh
+        ctx = lev = None
+        torch.cuda.empty_cache()
+        out["comparator"], out["sweep"] = run_sweeps(args, pmg, torch, flush, stream, hbm_peak, max_mhz, sm_count)
 
     if rank == 0 and world == 1 and not args.no_cpu:
         v, done, threads, tcpu = cpu_reference_run(args, 10 ** 6, 1, args.cpu_budget)

@@ -215,6 +215,21 @@ int64_t pmg_launch_count(void);
 int pmg_set_smoother_impl(int impl);
 int pmg_get_smoother_impl(void);
 
+/* Kernel organisation a colour launch of pmg_smooth runs on this level under
+ * the current implementation choice (introspection for the parity tests and
+ * the bench's roofline label): writes one of PMG_KERNEL_* to *kernel. */
+enum
+{
+  PMG_KERNEL_LINE = 0,    /* vp_smooth_kernel: seven 1D line stages, in place */
+  PMG_KERNEL_POINT = 1,   /* vp_point_kernel: degree 1, 3^d-point stencil */
+  PMG_KERNEL_PATCH2D = 2, /* vp_patch2d_kernel: 2D, one thread per patch */
+  PMG_KERNEL_PATCH3D = 3, /* vp_patch3d_kernel: 3D degree 2, one thread per patch */
+  PMG_KERNEL_PLANE = 4,   /* vp_smooth_plane_kernel: 3D degree <= 2, plane streaming */
+  PMG_KERNEL_PP = 5,      /* vp_smooth_pp_kernel: 3D, ping-pong conflict-free layouts */
+  PMG_KERNEL_NAIVE = 6    /* naive_smooth_kernel: the straightforward comparator */
+};
+int pmg_smoother_kernel(pmg_level h, int variant, int color, int *kernel);
+
 #ifdef __cplusplus
 }
 #endif

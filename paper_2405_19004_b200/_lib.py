@@ -64,6 +64,7 @@ SIGNATURES = [
     ("pmg_prolongate_slab", _i, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i, _vp]),
     ("pmg_l2_error_sin", _i, [_vp, _vp, _pd, _vp]),
     ("pmg_get_smoother_impl", _i, []),
+    ("pmg_smoother_kernel", _i, [_vp, _i, _i, _pi]),
 ]
 
 _lib = None

@@ -109,6 +109,8 @@ struct CachedGraph
   void *x = nullptr;
   const void *b = nullptr;
   int variant = -1, pre = -1, post = -1;
+  int impl = -1;        // smoother organisation the kernels were captured with
+  unsigned gen = ~0u;   // g_buf_generation at capture (workspace pointers)
 };
 
 struct pmg_mg_s
@@ -287,6 +289,7 @@ ColorArgs<T> color_args(const pmg_level_s *l, int color, T *x, const T *b)
   }
   a.mz = a.m;
   a.zoff = 0;
+  a.level_total = a.total;
   return a;
 }
 
@@ -515,8 +518,11 @@ void vcycle_entry(pmg_mg_s *mg, int li, T *x, const T *b, bool use_graph, cudaSt
     return;
   }
   CachedGraph &g = mg->graph;
+  // the key covers everything the captured launches baked in: vectors, level,
+  // variant, sweep counts, smoother organisation and workspace pointers
   if (!(g.exec && g.li == li && g.x == x && g.b == b && g.variant == mg->variant &&
-        g.pre == mg->pre && g.post == mg->post))
+        g.pre == mg->pre && g.post == mg->post && g.impl == smoother_impl_choice() &&
+        g.gen == g_buf_generation.load(std::memory_order_relaxed)))
   {
     if (g.exec)
     {
@@ -525,25 +531,39 @@ void vcycle_entry(pmg_mg_s *mg, int li, T *x, const T *b, bool use_graph, cudaSt
     }
     if (!mg->cap_stream)
       check_cuda(cudaStreamCreateWithFlags(&mg->cap_stream, cudaStreamNonBlocking), "stream");
-    // one eager pass first so lazy allocations / function attributes are set
-    // outside the capture; order it after the caller's stream
+    // the capture stream is not ordered after the caller's stream
     check_cuda(cudaStreamSynchronize(s), "graph pre-sync");
-    cudaGraph_t graph = nullptr;
-    check_cuda(cudaStreamBeginCapture(mg->cap_stream, cudaStreamCaptureModeRelaxed), "capture begin");
-    try
+    // a workspace (re)allocated while capturing (first use of a level) may
+    // invalidate pointers captured before it: capture again with the sizes
+    // settled (the second pass allocates nothing)
+    for (int pass = 0; pass < 2; ++pass)
     {
-      vcycle_impl<T>(mg, li, x, b, mg->cap_stream);
-    }
-    catch (...)
-    {
-      cudaStreamEndCapture(mg->cap_stream, &graph);
-      if (graph)
+      const unsigned gen0 = g_buf_generation.load(std::memory_order_relaxed);
+      cudaGraph_t graph = nullptr;
+      check_cuda(cudaStreamBeginCapture(mg->cap_stream, cudaStreamCaptureModeRelaxed), "capture begin");
+      try
+      {
+        vcycle_impl<T>(mg, li, x, b, mg->cap_stream);
+      }
+      catch (...)
+      {
+        cudaStreamEndCapture(mg->cap_stream, &graph);
+        if (graph)
+          cudaGraphDestroy(graph);
+        throw;
+      }
+      check_cuda(cudaStreamEndCapture(mg->cap_stream, &graph), "capture end");
+      if (g_buf_generation.load(std::memory_order_relaxed) != gen0 && pass == 0)
+      {
         cudaGraphDestroy(graph);
-      throw;
+        continue;
+      }
+      check_cuda(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
+      cudaGraphDestroy(graph);
+      break;
     }
-    check_cuda(cudaStreamEndCapture(mg->cap_stream, &graph), "capture end");
-    check_cuda(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
-    cudaGraphDestroy(graph);
+    g.impl = smoother_impl_choice();
+    g.gen = g_buf_generation.load(std::memory_order_relaxed);
     g.li = li;
     g.x = x;
     g.b = b;
@@ -882,6 +902,25 @@ int pmg_smooth_color(pmg_level h, int variant, int color, void *x, const void *b
   });
 }
 
+int pmg_smoother_kernel(pmg_level h, int variant, int color, int *kernel)
+{
+  return guard([&] {
+    require_level(h);
+    if (!kernel || color < 0 || color >= (1 << h->S.dim))
+      throw InvalidArg("smoother_kernel: invalid arguments");
+    if (variant == PMG_NAIVE)
+    {
+      *kernel = PMG_KERNEL_NAIVE;
+      return;
+    }
+    const int mode = variant == PMG_FUSED ? MODE_FUSED : variant == PMG_BOUNDARY ? MODE_BOUNDARY : MODE_SOLVE;
+    PMG_DISPATCH_T(h, {
+      const ColorArgs<T> a = color_args<T>(h, color, static_cast<T *>(nullptr), static_cast<const T *>(nullptr));
+      *kernel = ktab<T>(h).smooth_kernel(a, mode);
+    });
+  });
+}
+
 int pmg_smooth_color_slab(pmg_level h, int variant, int color, void *x_local, const void *b_local,
                           int64_t z_offset, int64_t nz_cells, int vz_lo, int vz_hi, void *stream)
 {
@@ -977,7 +1016,7 @@ int pmg_restrict_slab(pmg_level c, pmg_level f, const void *rf, int64_t zoff_f, 
       f->tB.ensure(static_cast<size_t>(mc * mc * np) * sizeof(T) + sizeof(T));
       ktab<T>(f).restrict_slab(f->prol_mats.data(), shift<T>(rf, zoff_f, mf * mf), shift<T>(rc, zoff_c, mc * mc),
                                mc, q0, q1, f->tA.as<T>() - pz0 * mc * mf, f->tB.as<T>() - pz0 * mc * mc,
-                               as_stream(stream));
+                               f->sm_count, as_stream(stream));
     });
   });
 }

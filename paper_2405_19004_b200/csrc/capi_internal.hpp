@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -18,6 +19,10 @@ struct DivergenceErr : std::runtime_error
 {
   using std::runtime_error::runtime_error;
 };
+
+// bumped whenever a DevBuf is (re)allocated: captured graphs that baked in
+// workspace pointers compare it before replaying
+inline std::atomic<unsigned> g_buf_generation{0};
 
 // RAII device buffer
 struct DevBuf
@@ -42,6 +47,7 @@ struct DevBuf
     bytes = 0;
     check_cuda(cudaMalloc(&p, b), "cudaMalloc");
     bytes = b;
+    g_buf_generation.fetch_add(1, std::memory_order_relaxed);
   }
   template <typename T>
   T *as() const

@@ -163,6 +163,9 @@ struct ColorArgs
   int np[3];      // patches of this colour per direction
   int vb[3];      // vertex coordinate v_a = 2 j_a + vb[a]
   int total;      // patches in this colour
+  int level_total;  // patches of this colour on the whole unit-cube level: kernel choice
+                    // (independent of slab / range restriction, so P slabs dispatch
+                    // exactly like one GPU and stay bitwise equal)
 };
 
 template <typename T>

@@ -12,6 +12,8 @@ struct KernelTable
 {
   // P: PatchMatsEO<T,K>*; mode: MODE_*
   void (*smooth)(const void *P, const ColorArgs<T> &a, int mode, int sm_count, cudaStream_t s) = nullptr;
+  // the organisation `smooth` launches for these arguments (PMG_KERNEL_*)
+  int (*smooth_kernel)(const ColorArgs<T> &a, int mode) = nullptr;
   // whole smoothing step in one persistent launch (3D fused / boundary, where
   // available): returns false when this (dim, degree) has no sweep kernel
   bool (*sweep)(const void *P, const SweepArgs<T> &sw, int mode, int sm_count, cudaStream_t s) = nullptr;
@@ -25,7 +27,7 @@ struct KernelTable
   void (*prolongate_slab)(const void *P, const T *xc, T *xf, bool acc, int64_t mc, int64_t f0, int64_t f1,
                           cudaStream_t s) = nullptr;
   void (*restrict_slab)(const void *P, const T *rf, T *rc, int64_t mc, int64_t q0, int64_t q1, T *tA, T *tB,
-                        cudaStream_t s) = nullptr;
+                        int sm_count, cudaStream_t s) = nullptr;
   // P: ProlMats<T,K>*
   void (*prolongate)(const void *P, const T *xc, T *xf, bool acc, int64_t mc, T *tA, T *tB,
                      int sm_count, cudaStream_t s) = nullptr;

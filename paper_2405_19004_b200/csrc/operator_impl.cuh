@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
 
   auto issue = [&](int it) {
     const int64_t q = zs - K + it;
-    const bool zin = q >= 0 && q < m;
+    // planes below zbeg - K feed only outputs below zbeg (never stored): not
+    // read, so a slab caller need only hold planes from zbeg - K
+    const bool zin = q >= 0 && q < m && q >= zbeg - K;
     T *dst = Xs + (it % 3) * XN;
     const T *xq = x + (zin ? q : 0) * m2;
 #pragma unroll

@@ -758,13 +758,13 @@ inline void restrict_slab_fine_range(int K, int64_t mc, int64_t q0, int64_t q1, 
 // per fine plane of [pz0, pz1) (global-plane bases, as the vectors)
 template <int K, typename T>
 void launch_restrict_slab(const ProlMats<T, K> &P, const T *rf, T *rc, int64_t mc, int64_t q0, int64_t q1, T *tA,
-                          T *tB, cudaStream_t s)
+                          T *tB, int sm_count, cudaStream_t s)
 {
   if (q1 <= q0)
     return;
   if (use_restrict3d<K>(mc))
   {
-    launch_restrict3d<K, T>(P, rf, rc, static_cast<T *>(nullptr), mc, q0, q1, 148, s);
+    launch_restrict3d<K, T>(P, rf, rc, static_cast<T *>(nullptr), mc, q0, q1, sm_count, s);
     return;
   }
   const int64_t mf = 2 * mc + 1;

@@ -37,7 +37,7 @@ __all__ = [
     "apply_laplacian", "compute_residual", "prolongate", "restrict_vector", "v_cycle",
     "full_multigrid", "FmgStats", "vector_norm", "compute_rhs", "l2_error", "gmres", "SolveStats",
     "DivergenceError", "set_smoother_impl", "get_smoother_impl", "compute_rhs_device",
-    "compute_residual_slab", "restrict_slab", "prolongate_slab",
+    "compute_residual_slab", "restrict_slab", "prolongate_slab", "smoother_kernel", "KERNEL_NAMES",
 ]
 
 _SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2, "sweep": 3, "patch": 4}
@@ -57,6 +57,19 @@ def set_smoother_impl(impl: str = "auto") -> None:
 def get_smoother_impl() -> str:
     code = _lib.load().pmg_get_smoother_impl()
     return {v: k for k, v in _SMOOTHER_IMPLS.items()}[code]
+
+
+KERNEL_NAMES = {0: "vp_smooth_kernel", 1: "vp_point_kernel", 2: "vp_patch2d_kernel", 3: "vp_patch3d_kernel",
+                4: "vp_smooth_plane_kernel", 5: "vp_smooth_pp_kernel", 6: "naive_smooth_kernel"}
+
+
+def smoother_kernel(ctx, variant="fused", color: int = 0) -> str:
+    """Name of the kernel a colour launch of smooth() runs on this level under
+    the current set_smoother_impl choice (pmg_smoother_kernel)."""
+    out = ctypes.c_int(-1)
+    check(_lib.load().pmg_smoother_kernel(ctx.handle, _variant_code(variant), int(color), ctypes.byref(out)),
+          "smoother_kernel")
+    return KERNEL_NAMES[out.value]
 
 
 class SmootherVariant:
@@ -172,10 +185,24 @@ class _Arr:
             self.obj = a
 
 
-def _stream(arrs) -> ctypes.c_void_p:
+def _stream(arrs, ctx=None) -> ctypes.c_void_p:
+    """torch's current stream ON THE DEVICE of the vectors; every device vector
+    must live on one device, and on the context's device when one is given
+    (the C-ABI dereferences them on that device)."""
     import torch
 
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    devs = set()
+    for a in arrs:
+        t = a.obj if isinstance(a, _Arr) else a
+        if _is_torch(t) and t.is_cuda:
+            devs.add(t.device.index if t.device.index is not None else torch.cuda.current_device())
+    if len(devs) > 1:
+        raise ValueError(f"vectors on different CUDA devices {sorted(devs)}")
+    want = getattr(ctx, "device", None) if ctx is not None else None
+    if want is not None and devs and devs != {want}:
+        raise ValueError(f"vectors on cuda:{devs.pop()} but the context lives on cuda:{want}")
+    dev = devs.pop() if devs else (want if want is not None else torch.cuda.current_device())
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
 
 
 def _same_kind(*arrs):
@@ -261,7 +288,7 @@ def smooth(ctx: LevelContext, x, b, variant="fused", threads: int = 1, ws=None) 
     v = _variant_code(variant)
     lib = _lib.load()
     if _same_kind(xa, ba):
-        check(lib.pmg_smooth(ctx.handle, v, xa.ptr, ba.ptr, _stream((xa, ba))), "smooth")
+        check(lib.pmg_smooth(ctx.handle, v, xa.ptr, ba.ptr, _stream((xa, ba), ctx)), "smooth")
     else:
         check(lib.pmg_smooth_host(ctx.handle, v, xa.ptr, ba.ptr), "smooth")
 
@@ -274,7 +301,7 @@ def smooth_color(ctx: LevelContext, color: int, x, b, variant="fused") -> None:
     if not (xa.device and ba.device):
         raise ValueError("smooth_color: device (torch CUDA) vectors only")
     check(_lib.load().pmg_smooth_color(ctx.handle, _variant_code(variant), color, xa.ptr, ba.ptr,
-                                       _stream((xa, ba))), "smooth_color")
+                                       _stream((xa, ba), ctx)), "smooth_color")
 
 
 def smooth_color_slab(ctx: LevelContext, color: int, x_local, b_local, z_offset: int, nz_cells: int,
@@ -290,7 +317,7 @@ def smooth_color_slab(ctx: LevelContext, color: int, x_local, b_local, z_offset:
     ba = _Arr(b_local, b_local.numel(), ctx._code, "b_local", False)
     check(_lib.load().pmg_smooth_color_slab(ctx.handle, _variant_code(variant), color, xa.ptr, ba.ptr,
                                             int(z_offset), int(nz_cells), int(vz_lo), int(vz_hi),
-                                            _stream((xa,))), "smooth_color_slab")
+                                            _stream((xa,), ctx)), "smooth_color_slab")
 
 
 def apply_laplacian(ctx: LevelContext, x, y, mode: str = "colored", threads: int = 1) -> None:
@@ -300,7 +327,7 @@ def apply_laplacian(ctx: LevelContext, x, y, mode: str = "colored", threads: int
     ya = _Arr(y, n, ctx._code, "y", True)
     lib = _lib.load()
     if _same_kind(xa, ya):
-        check(lib.pmg_apply_laplacian(ctx.handle, xa.ptr, ya.ptr, _stream((xa, ya))), "apply_laplacian")
+        check(lib.pmg_apply_laplacian(ctx.handle, xa.ptr, ya.ptr, _stream((xa, ya), ctx)), "apply_laplacian")
     else:
         check(lib.pmg_apply_laplacian_host(ctx.handle, xa.ptr, ya.ptr), "apply_laplacian")
 
@@ -313,7 +340,7 @@ def compute_residual(ctx: LevelContext, x, b, r, threads: int = 1) -> None:
     ra = _Arr(r, n, ctx._code, "r", True)
     lib = _lib.load()
     if _same_kind(xa, ba, ra):
-        check(lib.pmg_compute_residual(ctx.handle, xa.ptr, ba.ptr, ra.ptr, _stream((xa,))), "compute_residual")
+        check(lib.pmg_compute_residual(ctx.handle, xa.ptr, ba.ptr, ra.ptr, _stream((xa, ba, ra), ctx)), "compute_residual")
     else:
         check(lib.pmg_compute_residual_host(ctx.handle, xa.ptr, ba.ptr, ra.ptr), "compute_residual")
 
@@ -332,7 +359,7 @@ def prolongate(coarse: LevelContext, fine: LevelContext, x_coarse, x_fine, accum
     lib = _lib.load()
     if _same_kind(xc, xf):
         check(lib.pmg_prolongate(coarse.handle, fine.handle, xc.ptr, xf.ptr, int(accumulate),
-                                 _stream((xc,))), "prolongate")
+                                 _stream((xc, xf), fine)), "prolongate")
     else:
         if accumulate:
             raise ValueError("prolongate: accumulate needs device vectors")
@@ -346,7 +373,7 @@ def restrict_vector(coarse: LevelContext, fine: LevelContext, r_fine, r_coarse) 
     rc = _Arr(r_coarse, coarse.level.total_dofs, fine._code, "r_coarse", True)
     lib = _lib.load()
     if _same_kind(rf, rc):
-        check(lib.pmg_restrict_vector(coarse.handle, fine.handle, rf.ptr, rc.ptr, _stream((rf,))),
+        check(lib.pmg_restrict_vector(coarse.handle, fine.handle, rf.ptr, rc.ptr, _stream((rf, rc), fine)),
               "restrict_vector")
     else:
         check(lib.pmg_restrict_vector_host(coarse.handle, fine.handle, rf.ptr, rc.ptr), "restrict_vector")
@@ -375,7 +402,8 @@ def compute_residual_slab(ctx: LevelContext, x, b, r, zoff: int, p0: int, p1: in
     ar, nr = _slab(ctx, r, "r", True)
     if not n == nb == nr:
         raise ValueError("compute_residual_slab: x, b, r must hold the same planes")
-    check(_lib.load().pmg_compute_residual_slab(ctx.handle, ax.ptr, ab.ptr, ar.ptr, zoff, n, p0, p1, _stream([x])),
+    check(_lib.load().pmg_compute_residual_slab(ctx.handle, ax.ptr, ab.ptr, ar.ptr, zoff, n, p0, p1,
+                                                _stream([x, b, r], ctx)),
           "compute_residual_slab")
 
 
@@ -385,7 +413,7 @@ def restrict_slab(coarse: LevelContext, fine: LevelContext, rf, zoff_f: int, rc,
     af, nf = _slab(fine, rf, "rf", False)
     ac, nc = _slab(coarse, rc, "rc", True)
     check(_lib.load().pmg_restrict_slab(coarse.handle, fine.handle, af.ptr, zoff_f, nf, ac.ptr, zoff_c, nc, q0, q1,
-                                        _stream([rf])), "restrict_slab")
+                                        _stream([rf, rc], fine)), "restrict_slab")
 
 
 def prolongate_slab(coarse: LevelContext, fine: LevelContext, xc, zoff_c: int, xf, zoff_f: int, f0: int, f1: int,
@@ -394,7 +422,7 @@ def prolongate_slab(coarse: LevelContext, fine: LevelContext, xc, zoff_c: int, x
     ac, nc = _slab(coarse, xc, "xc", False)
     af, nf = _slab(fine, xf, "xf", True)
     check(_lib.load().pmg_prolongate_slab(coarse.handle, fine.handle, ac.ptr, zoff_c, nc, af.ptr, zoff_f, nf, f0, f1,
-                                          1 if accumulate else 0, _stream([xf])), "prolongate_slab")
+                                          1 if accumulate else 0, _stream([xc, xf], fine)), "prolongate_slab")
 
 
 def vector_norm(v, device: int = 0) -> float:
@@ -496,7 +524,8 @@ def v_cycle(ctx: MultigridContext, li: int, x, b, use_graph: bool = False) -> No
     ba = _Arr(b, n, lev._code, "b", False)
     lib = _lib.load()
     if _same_kind(xa, ba):
-        check(lib.pmg_v_cycle(ctx.handle, li, xa.ptr, ba.ptr, int(use_graph), _stream((xa,))), "v_cycle")
+        check(lib.pmg_v_cycle(ctx.handle, li, xa.ptr, ba.ptr, int(use_graph), _stream((xa, ba), ctx.levels[-1])),
+              "v_cycle")
     else:
         check(lib.pmg_v_cycle_host(ctx.handle, li, xa.ptr, ba.ptr), "v_cycle")
 
@@ -536,7 +565,7 @@ def full_multigrid(ctx: MultigridContext, rhs_per_level, x, tol: float, max_iter
     st = _lib.load().pmg_full_multigrid(
         ctx.handle, ptrs, ctypes.c_void_p(xd.data_ptr()), float(tol), int(max_iterations), ctypes.byref(its),
         hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap,
-        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
     history = [float(h) for h in hist[: its.value + 1]]
     check(st, "full_multigrid", history)
     if host_x:
@@ -564,7 +593,7 @@ def compute_rhs_device(ctx: LevelContext, f: str, out) -> None:
     if f not in kinds:
         raise ValueError("compute_rhs: f must be 'one' or 'sin'")
     a = _Arr(out, ctx.level.total_dofs, ctx._code, "b", True)
-    check(_lib.load().pmg_compute_rhs(ctx.handle, kinds[f], a.ptr, _stream([out])), "compute_rhs")
+    check(_lib.load().pmg_compute_rhs(ctx.handle, kinds[f], a.ptr, _stream([out], ctx)), "compute_rhs")
 
 
 def l2_error(level, x, u_exact: str = "sin") -> float:
@@ -576,7 +605,7 @@ def l2_error(level, x, u_exact: str = "sin") -> float:
     if isinstance(level, LevelContext) and _is_torch(x) and x.is_cuda:
         a = _Arr(x, level.level.total_dofs, level._code, "x", False)
         out = ctypes.c_double()
-        check(_lib.load().pmg_l2_error_sin(level.handle, a.ptr, ctypes.byref(out), _stream([x])), "l2_error")
+        check(_lib.load().pmg_l2_error_sin(level.handle, a.ptr, ctypes.byref(out), _stream([x], level)), "l2_error")
         return out.value
     if isinstance(level, LevelContext):
         level = level.level
@@ -628,7 +657,7 @@ def gmres(op_ctx: MultigridContext, prec_ctx: MultigridContext, b, x, tol: float
     st = _lib.load().pmg_gmres(op_ctx.handle, prec_ctx.handle, ctypes.c_void_p(bd.data_ptr()),
                                ctypes.c_void_p(xd.data_ptr()), float(tol), int(restart), int(max_iterations),
                                ctypes.byref(its), hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap,
-                               ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+                               ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t0
     h = [float(v) for v in hist if not np.isnan(v)]
