@@ -421,8 +421,15 @@ bool sweep_impl(pmg_level_s *l, int variant, T *x, const T *b, cudaStream_t s)
   const size_t need = static_cast<size_t>(2 + sw.ncolors * sw.nv) * sizeof(int);
   if (l->sweep_sync.bytes < need)
   {
+    // zeroed now, not on `s`: `s` may be a capture stream whose first graph
+    // is discarded after an allocation (vcycle_entry), and the kernel keeps
+    // the counters at zero between launches itself
     l->sweep_sync.ensure(need);
-    check_cuda(cudaMemsetAsync(l->sweep_sync.p, 0, need, s), "sweep counters");
+    cudaStream_t z = nullptr;
+    check_cuda(cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking), "stream");
+    check_cuda(cudaMemsetAsync(l->sweep_sync.p, 0, need, z), "sweep counters");
+    check_cuda(cudaStreamSynchronize(z), "sweep counters");
+    cudaStreamDestroy(z);
   }
   sw.sync = l->sweep_sync.as<int>();
   return kt.sweep(l->patch_mats.data(), sw, variant == PMG_FUSED ? MODE_FUSED : MODE_BOUNDARY, l->sm_count, s);
