@@ -202,6 +202,79 @@ int pmg_restrict_slab(pmg_level coarse, pmg_level fine, const void *rf, int64_t 
 int pmg_prolongate_slab(pmg_level coarse, pmg_level fine, const void *xc, int64_t zoff_c, int64_t np_c, void *xf,
                         int64_t zoff_f, int64_t np_f, int64_t f0, int64_t f1, int accumulate, void *stream);
 
+/* ---- multi-GPU: slab domain decomposition behind the C-ABI ----------------
+ * ~ make_multigrid_context / smooth / v_cycle / full_multigrid
+ *   (multigrid.hpp:51-86, smoother.hpp:45-47) on `world` ranks, one device
+ *   per rank. 3D only (dim must be 3 when world > 1). Rank g owns a
+ *   contiguous range of patch-vertex planes along z:
+ *   per colour one one-directional k-plane message per interface, posted after
+ *   the boundary-layer patches and overlapped with the interior ones; the
+ *   V-cycle adds one halo exchange per residual / restriction / coarse
+ *   correction, and levels too thin to split are agglomerated on rank 0
+ *   (coarse right-hand side gathered, coarse V-cycle as one CUDA graph,
+ *   correction broadcast). Colour order and per-patch arithmetic are those of
+ *   one device, so smoother and V-cycle results equal the single-device ones
+ *   bitwise; norms are all-reduced (rank-ordered partial sums).
+ *
+ * Transports: PMG_DD_COPY — all ranks in this process, plane messages as
+ *   device-to-device / peer copies (cudaMemcpyPeerAsync, NVLink when the
+ *   devices are peers); device ids may repeat ("virtual ranks" on one GPU).
+ *   PMG_DD_NCCL — grouped ncclSend/ncclRecv, ncclBroadcast, ncclAllReduce
+ *   (libnccl.so.2 loaded at first use): pmg_dd_create with distinct devices
+ *   (ncclCommInitAll), or pmg_dd_create_rank in one process per GPU
+ *   (ncclCommInitRank with the id rank 0 got from pmg_dd_nccl_id).
+ *
+ * stack > 1 builds a box of `stack` unit cubes along z (weak scaling: one
+ * cube per rank); only pmg_dd_smooth is defined on such a box.
+ * Vectors: the handle owns x and b of the finest level, as per-rank slabs of
+ * GLOBAL dof planes [z0, z0 + nplanes) (m*m values per plane, the reference
+ * layout otherwise); a rank owns planes [own_lo, own_hi]. Operations enqueue
+ * on the ranks' streams (pmg_dd_stream) and return; pmg_dd_synchronize waits. */
+typedef struct pmg_dd_s *pmg_dd;
+enum
+{
+  PMG_DD_COPY = 0,
+  PMG_DD_NCCL = 1
+};
+enum
+{
+  PMG_DD_X = 0,
+  PMG_DD_B = 1
+};
+int pmg_dd_create(int ndev, const int *devices, int dim, int degree, int finest_level, int stack,
+                  int dtype, int variant, int transport, pmg_dd *out);
+/* NCCL unique id (NCCL_UNIQUE_ID_BYTES = 128 bytes), made once on rank 0 and
+ * shared with the other processes by the caller. */
+int pmg_dd_nccl_id(void *id_out);
+int pmg_dd_create_rank(int world, int rank, int device, const void *nccl_id, int dim, int degree,
+                       int finest_level, int stack, int dtype, int variant, pmg_dd *out);
+int pmg_dd_destroy(pmg_dd h);
+/* world size, ranks held by this process, number of decomposed levels
+ * (finest first; 0 = every level is agglomerated on rank 0). */
+int pmg_dd_info(pmg_dd h, int *world, int *local_ranks, int *decomposed_levels);
+/* Local rank i's slab of the finest-level vector `which` (PMG_DD_X / _B). */
+int pmg_dd_slab(pmg_dd h, int local, int which, void **ptr, int64_t *z0, int64_t *nplanes,
+                int64_t *own_lo, int64_t *own_hi);
+/* The compute stream of local rank i (cudaStream_t) and its global rank. */
+int pmg_dd_stream(pmg_dd h, int local, void **stream, int *rank);
+/* Global host vector (N = m*m*mz values) <-> the local ranks' slabs:
+ * scatter fills each slab completely, gather writes the owned planes. */
+int pmg_dd_scatter_host(pmg_dd h, int which, const void *global);
+int pmg_dd_gather_host(pmg_dd h, int which, void *global);
+int pmg_dd_set_smoothing(pmg_dd h, int pre_smooth, int post_smooth);
+/* One smoothing step of the finest level (x in place). */
+int pmg_dd_smooth(pmg_dd h);
+/* One V-cycle from the finest level (x in place, b right-hand side). */
+int pmg_dd_v_cycle(pmg_dd h);
+/* ||b - A x|| of the finest level (all-reduced; synchronises). */
+int pmg_dd_residual_norm(pmg_dd h, double *out);
+/* ~ full_multigrid (multigrid.cpp:355-400), f64 only: rhs_host[li] is the
+ * global host right-hand side of level index li (li = 0 .. finest-1; every
+ * process passes all of them); the solution is left in the x slabs. */
+int pmg_dd_full_multigrid(pmg_dd h, const double *const *rhs_host, double tol, int max_iterations,
+                          int *iterations, double *history, int history_cap);
+int pmg_dd_synchronize(pmg_dd h);
+
 /* Number of kernel launches issued by this library since load (counter). */
 int64_t pmg_launch_count(void);
 

@@ -65,6 +65,21 @@ SIGNATURES = [
     ("pmg_l2_error_sin", _i, [_vp, _vp, _pd, _vp]),
     ("pmg_get_smoother_impl", _i, []),
     ("pmg_smoother_kernel", _i, [_vp, _i, _i, _pi]),
+    ("pmg_dd_create", _i, [_i, _pi, _i, _i, _i, _i, _i, _i, _i, ctypes.POINTER(_vp)]),
+    ("pmg_dd_nccl_id", _i, [_vp]),
+    ("pmg_dd_create_rank", _i, [_i, _i, _i, _vp, _i, _i, _i, _i, _i, _i, ctypes.POINTER(_vp)]),
+    ("pmg_dd_destroy", _i, [_vp]),
+    ("pmg_dd_info", _i, [_vp, _pi, _pi, _pi]),
+    ("pmg_dd_slab", _i, [_vp, _i, _i, ctypes.POINTER(_vp), _pi64, _pi64, _pi64, _pi64]),
+    ("pmg_dd_stream", _i, [_vp, _i, ctypes.POINTER(_vp), _pi]),
+    ("pmg_dd_scatter_host", _i, [_vp, _i, _vp]),
+    ("pmg_dd_gather_host", _i, [_vp, _i, _vp]),
+    ("pmg_dd_set_smoothing", _i, [_vp, _i, _i]),
+    ("pmg_dd_smooth", _i, [_vp]),
+    ("pmg_dd_v_cycle", _i, [_vp]),
+    ("pmg_dd_residual_norm", _i, [_vp, _pd]),
+    ("pmg_dd_full_multigrid", _i, [_vp, ctypes.POINTER(_vp), _d, _i, _pi, _pd, _i]),
+    ("pmg_dd_synchronize", _i, [_vp]),
 ]
 
 _lib = None

@@ -38,6 +38,7 @@ __all__ = [
     "full_multigrid", "FmgStats", "vector_norm", "compute_rhs", "l2_error", "gmres", "SolveStats",
     "DivergenceError", "set_smoother_impl", "get_smoother_impl", "compute_rhs_device",
     "compute_residual_slab", "restrict_slab", "prolongate_slab", "smoother_kernel", "KERNEL_NAMES",
+    "MultiGpuContext", "nccl_unique_id",
 ]
 
 _SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2, "sweep": 3, "patch": 4}
@@ -667,3 +668,131 @@ def gmres(op_ctx: MultigridContext, prec_ctx: MultigridContext, b, x, tol: float
     if host_x:
         np.copyto(x, xd.cpu().numpy())
     return SolveStats(its.value, h, None, wall)
+
+
+# ---------------------------------------------------------------------------
+# Multi-GPU (the C-ABI's slab domain decomposition, pmg_dd_*; csrc/dd.cu)
+# ---------------------------------------------------------------------------
+DD_TRANSPORTS = {"copy": 0, "nccl": 1}
+
+
+class MultiGpuContext:
+    """make_multigrid_context + smooth / v_cycle / full_multigrid
+    (multigrid.hpp:51-86) on a z-slab decomposition over several devices,
+    driven by the C++ host code of the library (one process).
+
+    devices: one device id per rank (repeats allowed with transport "copy":
+    virtual ranks sharing a GPU). The handle owns x and b of the finest
+    level; `scatter` / `gather` move global host vectors in and out.
+    Results equal the single-device ones bitwise (norms to rounding)."""
+
+    def __init__(self, devices, dim: int, degree: int, finest_level: int, stack: int = 1,
+                 dtype=np.float64, variant="fused", transport: str = "copy", _handle=None):
+        lib = _lib.load()
+        self.dim, self.degree, self.finest_level, self.stack = dim, degree, finest_level, stack
+        self.dtype = np.dtype(dtype)
+        m = (1 << finest_level) * degree - 1
+        self.mz = stack * (1 << finest_level) * degree - 1
+        self.total_dofs = m * m * self.mz
+        if _handle is not None:
+            self._h = _handle
+        else:
+            if transport not in DD_TRANSPORTS:
+                raise ValueError(f"transport must be one of {sorted(DD_TRANSPORTS)}")
+            devs = (ctypes.c_int * len(devices))(*devices)
+            h = ctypes.c_void_p()
+            check(lib.pmg_dd_create(len(devices), devs, dim, degree, finest_level, stack, _dtype_code(dtype),
+                                    _variant_code(variant), DD_TRANSPORTS[transport], ctypes.byref(h)),
+                  "MultiGpuContext")
+            self._h = h
+        w, lr, nd = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        check(lib.pmg_dd_info(self._h, ctypes.byref(w), ctypes.byref(lr), ctypes.byref(nd)), "dd_info")
+        self.world, self.local_ranks, self.decomposed_levels = w.value, lr.value, nd.value
+
+    @classmethod
+    def for_rank(cls, world: int, rank: int, device: int, nccl_id: bytes, dim: int, degree: int,
+                 finest_level: int, stack: int = 1, dtype=np.float64, variant="fused"):
+        """One process per GPU over NCCL (nccl_id from `nccl_unique_id()` on
+        rank 0, shared by the caller, e.g. torch.distributed)."""
+        lib = _lib.load()
+        buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        h = ctypes.c_void_p()
+        check(lib.pmg_dd_create_rank(world, rank, device, buf, dim, degree, finest_level, stack,
+                                     _dtype_code(dtype), _variant_code(variant), ctypes.byref(h)),
+              "MultiGpuContext.for_rank")
+        return cls(None, dim, degree, finest_level, stack, dtype, variant, _handle=h)
+
+    def slab(self, local: int = 0, which: str = "x"):
+        """(device pointer, first global plane, planes, own_lo, own_hi)."""
+        p = ctypes.c_void_p()
+        z0, np_, lo, hi = (ctypes.c_int64() for _ in range(4))
+        check(_lib.load().pmg_dd_slab(self._h, local, 0 if which == "x" else 1, ctypes.byref(p), ctypes.byref(z0),
+                                      ctypes.byref(np_), ctypes.byref(lo), ctypes.byref(hi)), "dd_slab")
+        return p.value, z0.value, np_.value, lo.value, hi.value
+
+    def stream(self, local: int = 0):
+        """(cudaStream_t of local rank `local`, its global rank)."""
+        s, r = ctypes.c_void_p(), ctypes.c_int()
+        check(_lib.load().pmg_dd_stream(self._h, local, ctypes.byref(s), ctypes.byref(r)), "dd_stream")
+        return s.value, r.value
+
+    def _host(self, a, writable):
+        if not isinstance(a, np.ndarray) or a.dtype != self.dtype or a.size != self.total_dofs \
+                or not a.flags.c_contiguous or (writable and not a.flags.writeable):
+            raise ValueError(f"expected a contiguous {self.dtype} host array of {self.total_dofs} values")
+        return ctypes.c_void_p(a.ctypes.data)
+
+    def scatter(self, which: str, global_host: np.ndarray) -> None:
+        check(_lib.load().pmg_dd_scatter_host(self._h, 0 if which == "x" else 1, self._host(global_host, False)),
+              "dd_scatter")
+
+    def gather(self, which: str = "x", out: np.ndarray | None = None) -> np.ndarray:
+        out = np.zeros(self.total_dofs, dtype=self.dtype) if out is None else out
+        check(_lib.load().pmg_dd_gather_host(self._h, 0 if which == "x" else 1, self._host(out, True)), "dd_gather")
+        return out
+
+    def set_smoothing(self, pre: int, post: int) -> None:
+        check(_lib.load().pmg_dd_set_smoothing(self._h, pre, post), "dd_set_smoothing")
+
+    def smooth(self) -> None:
+        check(_lib.load().pmg_dd_smooth(self._h), "dd_smooth")
+
+    def v_cycle(self) -> None:
+        check(_lib.load().pmg_dd_v_cycle(self._h), "dd_v_cycle")
+
+    def residual_norm(self) -> float:
+        out = ctypes.c_double()
+        check(_lib.load().pmg_dd_residual_norm(self._h, ctypes.byref(out)), "dd_residual_norm")
+        return out.value
+
+    def full_multigrid(self, rhs_per_level, tol: float, max_iterations: int = 100) -> FmgStats:
+        """Alg. 2 on the decomposition (f64); the solution stays in x
+        (`gather("x")`). rhs_per_level: global host arrays, one per level."""
+        L = self.finest_level
+        if len(rhs_per_level) != L:
+            raise ValueError("full_multigrid: need one rhs per level")
+        arrs = [np.ascontiguousarray(r, dtype=np.float64) for r in rhs_per_level]
+        ptrs = (ctypes.c_void_p * L)(*[a.ctypes.data for a in arrs])
+        cap = max_iterations + 2
+        hist = np.full(cap, np.nan)
+        its = ctypes.c_int(0)
+        st = _lib.load().pmg_dd_full_multigrid(self._h, ptrs, float(tol), int(max_iterations), ctypes.byref(its),
+                                              hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap)
+        history = [float(h) for h in hist[: its.value + 1]]
+        check(st, "full_multigrid", history)
+        return FmgStats(its.value, history)
+
+    def synchronize(self) -> None:
+        check(_lib.load().pmg_dd_synchronize(self._h), "dd_synchronize")
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib._lib is not None:
+            _lib._lib.pmg_dd_destroy(self._h)
+            self._h = None
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0 of MultiGpuContext.for_rank)."""
+    buf = ctypes.create_string_buffer(128)
+    check(_lib.load().pmg_dd_nccl_id(buf), "nccl_unique_id")
+    return buf.raw

@@ -1,0 +1,144 @@
+"""GPU: the multi-GPU C-ABI (pmg_dd_*, csrc/dd.cu) — C++ host code driving the
+slab decomposition. On this one-GPU box P "virtual ranks" share the device
+(transport PMG_DD_COPY, the same event / copy schedule a multi-device run
+uses with peer copies): smoother step and V-cycle equal the single-device
+ones bitwise, full multigrid takes the same number of V-cycles. The NCCL
+transport runs with one rank (ncclCommInitAll / ncclCommInitRank, grouped
+point-to-point, broadcast and all-reduce with a single participant)."""
+
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_cpp_dd_parity(cuda):
+    exe = os.path.join(ROOT, "tests", "cpp", "_bin", "dd_parity")
+    if not os.path.exists(exe):
+        pytest.fail("tests/cpp/_bin/dd_parity missing: run __graft_entry__.build()")
+    # (k, L, P, dtype): decomposed finest + agglomerated coarse, 2/4/8 ranks,
+    # f64 and f32, and a level too thin to split (the whole V-cycle on rank 0)
+    cases = [2, 5, 2, 0, 2, 6, 4, 0, 2, 7, 8, 0, 1, 8, 8, 0, 4, 6, 4, 0, 3, 6, 2, 0,
+             2, 6, 2, 1, 4, 5, 2, 1, 2, 4, 2, 0, 5, 4, 2, 0]
+    out = subprocess.run([exe, "0"] + [str(c) for c in cases], capture_output=True, text=True, timeout=900)
+    print(out.stdout, out.stderr)
+    assert out.returncode == 0, out.stdout + out.stderr
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("k=")]
+    assert len(lines) == len(cases) // 4 and all(ln.endswith("OK") for ln in lines)
+
+
+def _inputs(n, dtype, seed):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(-1, 1, n).astype(dtype), rng.uniform(-1, 1, n).astype(dtype)
+
+
+def _single(k, L, dtype, x0, b):
+    import torch
+
+    import paper_2405_19004_b200 as pmg
+
+    mg = pmg.make_multigrid_context(3, k, L, dtype=dtype)
+    xs = torch.from_numpy(x0.copy()).cuda()
+    bd = torch.from_numpy(b).cuda()
+    pmg.smooth(mg.levels[-1], xs, bd, "fused")
+    xv = torch.from_numpy(x0.copy()).cuda()
+    pmg.v_cycle(mg, L - 1, xv, bd)
+    torch.cuda.synchronize()
+    return xs.cpu().numpy(), xv.cpu().numpy()
+
+
+@pytest.mark.parametrize("variant", ["fused", "boundary"])
+def test_python_multigpu_context_bitwise(cuda, variant):
+    import paper_2405_19004_b200 as pmg
+
+    k, L, P = 2, 6, 3
+    ctx = pmg.MultiGpuContext([0] * P, 3, k, L, variant=variant)
+    assert ctx.world == P and ctx.local_ranks == P and ctx.decomposed_levels >= 1
+    x0, b = _inputs(ctx.total_dofs, np.float64, 5)
+    mg = pmg.make_multigrid_context(3, k, L, variant=variant)
+    import torch
+
+    xs = torch.from_numpy(x0.copy()).cuda()
+    bd = torch.from_numpy(b).cuda()
+    for _ in range(2):
+        pmg.smooth(mg.levels[-1], xs, bd, variant)
+    xv = torch.from_numpy(x0.copy()).cuda()
+    pmg.v_cycle(mg, L - 1, xv, bd)
+    torch.cuda.synchronize()
+    ctx.scatter("x", x0)
+    ctx.scatter("b", b)
+    ctx.smooth()
+    ctx.smooth()
+    assert np.array_equal(ctx.gather("x"), xs.cpu().numpy())
+    ctx.scatter("x", x0)
+    ctx.v_cycle()
+    assert np.array_equal(ctx.gather("x"), xv.cpu().numpy())
+
+
+@pytest.mark.parametrize("mode", ["init_all", "init_rank"])
+def test_nccl_transport_one_rank(cuda, mode):
+    import paper_2405_19004_b200 as pmg
+
+    k, L = 2, 6
+    if mode == "init_all":
+        ctx = pmg.MultiGpuContext([0], 3, k, L, transport="nccl")
+    else:
+        ctx = pmg.MultiGpuContext.for_rank(1, 0, 0, pmg.nccl_unique_id(), 3, k, L)
+    x0, b = _inputs(ctx.total_dofs, np.float64, 9)
+    xs, xv = _single(k, L, np.float64, x0, b)
+    ctx.scatter("x", x0)
+    ctx.scatter("b", b)
+    ctx.smooth()
+    assert np.array_equal(ctx.gather("x"), xs)
+    ctx.scatter("x", x0)
+    ctx.v_cycle()
+    assert np.array_equal(ctx.gather("x"), xv)
+    assert ctx.residual_norm() > 0
+
+
+def test_multigpu_fmg_matches_single_and_reference_counts(cuda):
+    import paper_2405_19004_b200 as pmg
+
+    k, L, P = 2, 6, 2
+    ctx = pmg.MultiGpuContext([0] * P, 3, k, L)
+    rhs = [pmg.compute_rhs(lev, "sin") for lev in pmg.build_hierarchy(3, k, L)]
+    st = ctx.full_multigrid(rhs, 1e-8)
+    mg = pmg.make_multigrid_context(3, k, L)
+    x = np.zeros(ctx.total_dofs)
+    st1 = pmg.full_multigrid(mg, rhs, x, 1e-8)
+    assert st.iterations == st1.iterations
+    np.testing.assert_allclose(st.residual_history, st1.residual_history, rtol=1e-9)
+    np.testing.assert_allclose(ctx.gather("x"), x, rtol=0, atol=1e-12 * np.abs(x).max())
+
+
+def test_stacked_box_smoother_runs(cuda):
+    """Weak-scaling box (stack = P unit cubes along z): the smoother steps;
+    the V-cycle is refused (unit cube only), like the reference's mesh."""
+    import paper_2405_19004_b200 as pmg
+
+    ctx = pmg.MultiGpuContext([0, 0], 3, 2, 4, stack=2)
+    x0, b = _inputs(ctx.total_dofs, np.float64, 3)
+    ctx.scatter("x", x0)
+    ctx.scatter("b", b)
+    ctx.smooth()
+    assert np.isfinite(ctx.gather("x")).all()
+    with pytest.raises(ValueError):
+        ctx.v_cycle()
+
+
+def test_dd_argument_errors(cuda):
+    import paper_2405_19004_b200 as pmg
+
+    with pytest.raises(ValueError):
+        pmg.MultiGpuContext([0, 0], 2, 2, 4)  # 3D only
+    with pytest.raises(ValueError):
+        pmg.MultiGpuContext([0, 0], 3, 2, 4, transport="nccl")  # NCCL: distinct devices
+    with pytest.raises(ValueError):
+        pmg.MultiGpuContext([0] * 8, 3, 2, 2)  # 3 vertex planes over 8 ranks
+    with pytest.raises(ValueError):
+        pmg.MultiGpuContext([0], 3, 2, 4, variant="global")
