@@ -362,21 +362,41 @@ def main():
             pmg.smooth(lev, x, b, args.variant)
 
         colour_patch_counts = [colour_patches(args.dim, args.level, c) for c in range(1 << args.dim)]
-    else:
+    elif not shared:
         # weak scaling: a stack of `world` unit cubes along z, one slab per
-        # rank, per-colour halo planes over NCCL overlapped with the interior
-        # patches (paper_2405_19004_b200/dd.py)
+        # GPU, driven by the library's C++ decomposition (pmg_dd_create_rank,
+        # csrc/dd.cu): per colour the boundary-layer patches, one grouped
+        # ncclSend/ncclRecv of k planes per interface on a side stream, the
+        # interior patches concurrently
+        nid = [pmg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        mctx = pmg.MultiGpuContext.for_rank(world, rank, local, nid[0], 3, args.degree, args.level, stack=world,
+                                            dtype=dt, variant=args.variant)
+        plan = dd.make_plan(world, rank, args.degree, args.level, stack=world)
+        N_total = plan.m * plan.m * plan.mz
+        x = mctx.slab_tensor(0, "x")
+        b = mctx.slab_tensor(0, "b")
+        x.copy_(torch.rand(x.numel(), dtype=tdt, device="cuda", generator=gen) * 2 - 1)
+        b.copy_(torch.rand(b.numel(), dtype=tdt, device="cuda", generator=gen) * 2 - 1)
+        torch.cuda.synchronize()
+        stream = torch.cuda.ExternalStream(mctx.stream(0)[0])
+
+        def step():
+            mctx.smooth()
+
+    else:
+        # PMG_DD_SHARED_GPU: the Python driver (dd.py) over gloo, ranks sharing cuda:0
         plan = dd.make_plan(world, rank, args.degree, args.level, stack=world)
         N_total = plan.m * plan.m * plan.mz
         x = torch.rand(plan.nplanes * plan.plane_size, dtype=tdt, device="cuda", generator=gen) * 2 - 1
         b = torch.rand(plan.nplanes * plan.plane_size, dtype=tdt, device="cuda", generator=gen) * 2 - 1
-        comm = dd.StagedComm(x, plan.plane_size) if shared else dd.TorchDistComm(x, plan.plane_size)
-        smoother = dd.SlabSmoother(plan, dd.gpu_kernel(lev, plan, x, b, args.variant), comm,
-                                   side_stream=None if shared else torch.cuda.Stream())
+        smoother = dd.SlabSmoother(plan, dd.gpu_kernel(lev, plan, x, b, args.variant),
+                                   dd.StagedComm(x, plan.plane_size))
 
         def step():
             smoother.smooth()
 
+    if world > 1:
         n = 1 << args.level
         colour_patch_counts = []
         for c in range(8):
@@ -398,52 +418,13 @@ def main():
         step()
     barrier()
 
-    # multi-GPU: capture the whole decomposed step (8 colour launches with their
-    # NCCL plane messages) in a CUDA graph, so the per-colour host overhead of
-    # the Python driver and torch.distributed disappears; verified bitwise
-    # against an eager step, eager fallback otherwise (PMG_DD_GRAPH=0 disables)
     timed_step, graph_info, per_step_launches = step, None, None
-    if world > 1 and not shared and os.environ.get("PMG_DD_GRAPH", "1") == "1":
-        x_save = x.clone()
-        step()
-        x_eager = x.clone()
-        x.copy_(x_save)
-        barrier()
-        ok, reason, g = 1.0, "", None
-        try:
-            l0 = lib.pmg_launch_count()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                step()
-            per_step_launches = lib.pmg_launch_count() - l0
-        except Exception as e:  # capture of the NCCL messages not supported here
-            ok, reason = 0.0, str(e)[:160]
-        torch.cuda.synchronize()
-        flag = torch.tensor([ok], device="cuda")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank replays, or none does
-        if flag.item() == 1.0:
-            x.copy_(x_save)
-            barrier()
-            g.replay()
-            barrier()
-            same = torch.tensor([1.0 if torch.equal(x, x_eager) else 0.0], device="cuda")
-            dist.all_reduce(same, op=dist.ReduceOp.MIN)
-            if same.item() == 1.0:
-                timed_step = g.replay
-                graph_info = {"cuda_graph": True, "launches_per_step": int(per_step_launches)}
-            else:
-                reason = "graph replay differs from the eager step"
-        if timed_step is step:
-            graph_info = {"cuda_graph": False, "reason": reason or "capture failed on another rank"}
-            per_step_launches = None
-        x.copy_(x_eager)
-        barrier()
 
     # ---- timed region: K steps, CUDA events per step, L2 flushed between ------
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = lib.pmg_launch_count()
     sampler = ClockSampler(local)
-    with sampler:
+    with sampler, torch.cuda.stream(stream):  # N > 1: the decomposition's compute stream
         barrier()
         for i in range(args.steps):
             flush.fill_(float(i))
@@ -572,12 +553,13 @@ def main():
         oh = torch.empty(own.numel(), dtype=tdt, pin_memory=True)
         barrier()
         t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            x.copy_(xh, non_blocking=True)
-            b.copy_(bh, non_blocking=True)
-            step()
-            oh.copy_(dd.owned_part(plan, x), non_blocking=True)
-            torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            for _ in range(e2e_steps):
+                x.copy_(xh, non_blocking=True)
+                b.copy_(bh, non_blocking=True)
+                step()
+                oh.copy_(dd.owned_part(plan, x), non_blocking=True)
+                torch.cuda.synchronize()
         t_e2e = (time.perf_counter() - t0) / e2e_steps
         h2d, d2h = (xh.numel() + bh.numel()) * word, oh.numel() * word
     if dist is not None:
@@ -590,7 +572,8 @@ def main():
         cfg["workload"] = (f"3D Q{args.degree} box of {world} stacked unit cubes (2^{args.level} cells/dir each), "
                            f"one {args.variant} smoother step, z-slab per GPU")
         cfg["dofs"] = N_total
-        cfg["parallelism"] = f"slab decomposition x{world} (NCCL halo planes per colour)"
+        cfg["parallelism"] = (f"slab decomposition x{world} (C++ pmg_dd_*, NCCL halo planes per colour)" if not shared
+                              else f"slab decomposition x{world} (dd.py over gloo, ranks sharing one GPU)")
         if graph_info is not None:
             cfg["dd_step"] = graph_info
     out = {
@@ -603,7 +586,7 @@ def main():
         "e2e": {"value": N_total / t_e2e, "unit": "DoF/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "api": "pmg_smooth_host (C-ABI, pinned host buffers)" if world == 1 else
-                       "slab H2D, SlabSmoother.smooth, owned-plane D2H (pinned)"},
+                       "slab H2D, pmg_dd_smooth (C-ABI), owned-plane D2H (pinned)"},
         "clocks": sampler.summary(), "gpu_launches": int(launches),
     }
     if vcycle is not None:

@@ -125,6 +125,20 @@ int pmg_norm2(const void *v, int64_t n, int dtype, int device, double *out, void
  *   threads)   multigrid.hpp:51-54 (kind = vertex_patch). */
 int pmg_mg_create(int dim, int degree, int finest_level, int dtype, int variant, int device,
                   pmg_mg *out);
+/* SmootherKind, multigrid.hpp:16-20 (same numbering). */
+enum
+{
+  PMG_VERTEX_PATCH = 0,
+  PMG_POINT_GS = 1
+};
+/* ~ make_multigrid_context<T>(dim, degree, finest_level, variant, kind,
+ *   threads)   multigrid.hpp:51-54 with the smoother kind: PMG_POINT_GS makes
+ *   the V-cycle smooth with one lexicographic point Gauss-Seidel sweep
+ *   (multigrid.cpp:286-300; f64 only -> PMG_ERR_INVALID; a level beyond the
+ *   reference's 1e7-nonzero CSR budget -> PMG_ERR_RUNTIME, operator.cpp:209-227).
+ *   The coarse solve stays the patch smoother's exact step, as in the reference. */
+int pmg_mg_create_kind(int dim, int degree, int finest_level, int dtype, int variant, int kind,
+                       int device, pmg_mg *out);
 int pmg_mg_destroy(pmg_mg h);
 int pmg_mg_num_levels(pmg_mg h);
 pmg_level pmg_mg_level(pmg_mg h, int li); /* borrowed; index 0 = mesh level 1 */
@@ -158,6 +172,20 @@ int pmg_l2_error_sin_host(int dim, int degree, int level, const double *x, doubl
  * points of every cell (x: device, the level's dtype). */
 int pmg_compute_rhs(pmg_level h, int kind, void *b, void *stream);
 int pmg_l2_error_sin(pmg_level h, const void *x, double *out, void *stream);
+
+/* ~ point_gauss_seidel(a, x, b)   smoother.hpp / smoother.cpp:160-166 with
+ *   a = assemble_sparse(level): one forward lexicographic Gauss-Seidel sweep
+ *   (sparse.cpp:31-47) of an f64 level, x in place. The device sweep uses the
+ *   Kronecker-sum structure of the level operator (no CSR) and the reference's
+ *   row order exactly (wavefronts of independent rows, csrc/gs.cu). */
+int pmg_point_gauss_seidel(pmg_level h, void *x, const void *b, void *stream);
+int pmg_point_gauss_seidel_host(pmg_level h, double *x, const double *b);
+/* ~ assemble_sparse(level)   operator.hpp / operator.cpp:194-281: the CSR
+ *   matrix of the level operator, rows and columns in the reference's order.
+ *   Host only. With row_ptr = cols = vals = NULL only *nnz is set; otherwise
+ *   the arrays hold N + 1, nnz and nnz entries. */
+int pmg_assemble_sparse_host(int dim, int degree, int level, int64_t *row_ptr, int32_t *cols,
+                             double *vals, int64_t *nnz);
 
 /* ---- mixed precision / Krylov (krylov.hpp:30-39) -------------------------
  * Right-preconditioned GMRES(restart) in f64 on the device with the V-cycle

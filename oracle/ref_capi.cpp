@@ -25,6 +25,7 @@
 #include "pmg/operator.hpp"
 #include "pmg/patches.hpp"
 #include "pmg/smoother.hpp"
+#include "pmg/sparse.hpp"
 
 using namespace pmg;
 
@@ -202,6 +203,60 @@ void *ref_mg_create(int dim, int k, int L, int prec, int variant, int threads)
   {
     return nullptr;
   }
+}
+
+// make_multigrid_context with a smoother kind (0 vertex_patch, 1 point_gs);
+// nullptr plus *status on the reference's exception
+void *ref_mg_create_kind(int dim, int k, int L, int prec, int variant, int kind, int threads, int *status)
+{
+  RefMg *h = nullptr;
+  *status = guard([&] {
+    auto *hh = new RefMg{prec};
+    try
+    {
+      if (prec == 0)
+        hh->d = new MultigridContext<double>(make_multigrid_context<double>(
+            dim, k, L, static_cast<SmootherVariant>(variant), static_cast<SmootherKind>(kind), threads));
+      else
+        hh->f = new MultigridContext<float>(make_multigrid_context<float>(
+            dim, k, L, static_cast<SmootherVariant>(variant), static_cast<SmootherKind>(kind), threads));
+    }
+    catch (...)
+    {
+      delete hh;
+      throw;
+    }
+    h = hh;
+  });
+  return h;
+}
+
+// point_gauss_seidel on the context's CSR matrix of level index li (f64)
+int ref_point_gs(void *p, int li, double *x, const double *b)
+{
+  auto *h = static_cast<RefMg *>(p);
+  return guard([&] {
+    auto &c = *h->d;
+    const auto n = c.levels[li].level.total_dofs;
+    point_gauss_seidel(c.gs_matrices.at(li), std::span<double>(x, n), std::span<const double>(b, n));
+  });
+}
+
+// assemble_sparse of the finest level of build_hierarchy(dim, k, level);
+// arrays NULL -> only *nnz
+int ref_assemble_sparse(int dim, int k, int level, int64_t *row_ptr, int32_t *cols, double *vals, int64_t *nnz)
+{
+  return guard([&] {
+    auto levels = build_hierarchy(dim, k, level);
+    CsrMatrix a = assemble_sparse(levels.back());
+    *nnz = a.nnz();
+    if (row_ptr && cols && vals)
+    {
+      std::memcpy(row_ptr, a.row_ptr.data(), a.row_ptr.size() * sizeof(int64_t));
+      std::memcpy(cols, a.cols.data(), a.cols.size() * sizeof(int32_t));
+      std::memcpy(vals, a.vals.data(), a.vals.size() * sizeof(double));
+    }
+  });
 }
 
 void ref_mg_destroy(void *p)

@@ -65,6 +65,10 @@ SIGNATURES = [
     ("pmg_l2_error_sin", _i, [_vp, _vp, _pd, _vp]),
     ("pmg_get_smoother_impl", _i, []),
     ("pmg_smoother_kernel", _i, [_vp, _i, _i, _pi]),
+    ("pmg_mg_create_kind", _i, [_i, _i, _i, _i, _i, _i, _i, ctypes.POINTER(_vp)]),
+    ("pmg_point_gauss_seidel", _i, [_vp, _vp, _vp, _vp]),
+    ("pmg_point_gauss_seidel_host", _i, [_vp, _pd, _pd]),
+    ("pmg_assemble_sparse_host", _i, [_i, _i, _i, _pi64, ctypes.POINTER(ctypes.c_int32), _pd, _pi64]),
     ("pmg_dd_create", _i, [_i, _pi, _i, _i, _i, _i, _i, _i, _i, ctypes.POINTER(_vp)]),
     ("pmg_dd_nccl_id", _i, [_vp]),
     ("pmg_dd_create_rank", _i, [_i, _i, _i, _vp, _i, _i, _i, _i, _i, _i, ctypes.POINTER(_vp)]),

@@ -22,6 +22,7 @@
 #include "naive.cuh"
 #include "setup.hpp"
 #include "capi_internal.hpp"
+#include <type_traits>
 
 namespace pmgb
 {
@@ -100,6 +101,7 @@ struct pmg_level_s
   DevBuf red;             // reduction partials + result (double)
   DevBuf io[3];           // staging for the *_host entry points
   cudaStream_t io_stream = nullptr;
+  std::shared_ptr<GsData> gs;  // point Gauss-Seidel data (gs.cu), built on first use
 };
 
 struct CachedGraph
@@ -116,6 +118,7 @@ struct CachedGraph
 struct pmg_mg_s
 {
   std::vector<pmg_level> levels;
+  int kind = PMG_VERTEX_PATCH;  // SmootherKind (multigrid.hpp:16-20)
   int dtype = PMG_F64;
   int device = 0;
   int variant = PMG_FUSED;
@@ -490,6 +493,22 @@ double norm_impl(pmg_level_s *l, const T *v, int64_t n, cudaStream_t s)
   return out;
 }
 
+// apply_smoother (multigrid.cpp:286-300): the patch smoother, or one
+// lexicographic point Gauss-Seidel sweep (f64 only) for kind == point_gs
+template <typename T>
+void apply_smoother(pmg_mg_s *mg, pmg_level_s *lev, T *x, const T *b, cudaStream_t s)
+{
+  if (mg->kind == PMG_POINT_GS)
+  {
+    if constexpr (std::is_same_v<T, double>)
+      gs_smooth(lev, x, b, s);
+    else
+      throw std::logic_error("point Gauss-Seidel requires f64");
+    return;
+  }
+  smooth_impl<T>(lev, mg->variant, x, b, s);
+}
+
 template <typename T>
 void vcycle_impl(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s)
 {
@@ -503,7 +522,7 @@ void vcycle_impl(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s)
   }
   pmg_level_s *crs = mg->levels[li - 1];
   for (int i = 0; i < mg->pre; ++i)
-    smooth_impl<T>(lev, mg->variant, x, b, s);
+    apply_smoother<T>(mg, lev, x, b, s);
   T *r = mg->r_ws[li]->as<T>();
   T *bc = mg->bc_ws[li]->as<T>();
   T *xc = mg->xc_ws[li]->as<T>();
@@ -513,7 +532,7 @@ void vcycle_impl(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s)
   vcycle_impl<T>(mg, li - 1, xc, bc, s);
   prolongate_impl<T>(crs, lev, xc, x, true, s);
   for (int i = 0; i < mg->post; ++i)
-    smooth_impl<T>(lev, mg->variant, x, b, s);
+    apply_smoother<T>(mg, lev, x, b, s);
 }
 
 template <typename T>
@@ -709,6 +728,10 @@ void GmresWork::ensure(int64_t n, int restart, bool mixed)
   flag = bflag.as<int>();
 }
 
+std::shared_ptr<GsData> &level_gs_slot(pmg_level l) { return l->gs; }
+const LevelSetup &level_setup(pmg_level l) { return l->S; }
+int level_dtype(pmg_level l) { return l->dtype; }
+int level_device(pmg_level l) { return l->device; }
 int mg_dtype(pmg_mg h) { return h->dtype; }
 int mg_device(pmg_mg h) { return h->device; }
 int mg_levels(pmg_mg h) { return static_cast<int>(h->levels.size()); }
@@ -1175,7 +1198,18 @@ int pmg_norm2(const void *v, int64_t n, int dtype, int device, double *out, void
 int pmg_mg_create(int dim, int degree, int finest_level, int dtype, int variant, int device,
                   pmg_mg *out)
 {
+  return pmg_mg_create_kind(dim, degree, finest_level, dtype, variant, PMG_VERTEX_PATCH, device, out);
+}
+
+int pmg_mg_create_kind(int dim, int degree, int finest_level, int dtype, int variant, int kind, int device,
+                       pmg_mg *out)
+{
   return guard([&] {
+    if (kind != PMG_VERTEX_PATCH && kind != PMG_POINT_GS)
+      throw InvalidArg("unknown smoother kind");
+    // multigrid.cpp:32-36 (std::invalid_argument)
+    if (kind == PMG_POINT_GS && dtype != PMG_F64)
+      throw InvalidArg("point Gauss-Seidel runs in f64 only");
     if (!out)
       throw InvalidArg("null output handle");
     if (finest_level < 1)
@@ -1184,6 +1218,7 @@ int pmg_mg_create(int dim, int degree, int finest_level, int dtype, int variant,
         variant != PMG_BOUNDARY && variant != PMG_NAIVE)
       throw InvalidArg("unknown smoother variant");
     auto mg = std::make_unique<pmg_mg_s>();
+    mg->kind = kind;
     mg->dtype = dtype;
     mg->device = device;
     mg->variant = variant;
@@ -1210,6 +1245,11 @@ int pmg_mg_create(int dim, int degree, int finest_level, int dtype, int variant,
           transfer_scratch<float>(mg->levels[li]);
       }
     }
+    // the reference assembles a CSR matrix per level (multigrid.cpp:37-41):
+    // same nonzero budget (std::runtime_error), front lists built up front
+    if (kind == PMG_POINT_GS)
+      for (auto *l : mg->levels)
+        gs_data(l);
     *out = mg.release();
   });
 }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -93,6 +94,14 @@ int capi_guard(F &&f)
     return capi_status_from_current_exception();
   }
 }
+
+struct GsData;  // point Gauss-Seidel front lists of a level (gs.cu)
+std::shared_ptr<GsData> &level_gs_slot(pmg_level l);
+const LevelSetup &level_setup(pmg_level l);
+int level_dtype(pmg_level l);
+int level_device(pmg_level l);
+void gs_smooth(pmg_level l, double *x, const double *b, cudaStream_t s);
+GsData *gs_data(pmg_level l);
 
 int mg_dtype(pmg_mg h);
 int mg_device(pmg_mg h);

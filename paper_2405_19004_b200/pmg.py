@@ -38,7 +38,7 @@ __all__ = [
     "full_multigrid", "FmgStats", "vector_norm", "compute_rhs", "l2_error", "gmres", "SolveStats",
     "DivergenceError", "set_smoother_impl", "get_smoother_impl", "compute_rhs_device",
     "compute_residual_slab", "restrict_slab", "prolongate_slab", "smoother_kernel", "KERNEL_NAMES",
-    "MultiGpuContext", "nccl_unique_id",
+    "MultiGpuContext", "nccl_unique_id", "point_gauss_seidel", "assemble_sparse", "SMOOTHER_KINDS",
 ]
 
 _SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2, "sweep": 3, "patch": 4}
@@ -500,19 +500,62 @@ class MultigridContext:
             self._h = None
 
 
+SMOOTHER_KINDS = {"vertex_patch": 0, "point_gs": 1}  # SmootherKind, multigrid.hpp:16-20
+
+
 def make_multigrid_context(dim: int, degree: int, finest_level: int, variant="fused",
                            kind: str = "vertex_patch", threads: int = 1, dtype=np.float64,
                            device: int = 0) -> MultigridContext:
-    """multigrid.hpp:51-54. kind must be vertex_patch (point Gauss-Seidel is
-    out of scope)."""
-    if kind != "vertex_patch":
-        raise ValueError("only the vertex-patch smoother is provided on the GPU")
+    """multigrid.hpp:51-54. kind "point_gs" smooths with one lexicographic
+    point Gauss-Seidel sweep per pre/post step (f64 only, like the reference;
+    ValueError otherwise; RuntimeError past the reference's 1e7-nonzero CSR
+    budget)."""
+    if kind not in SMOOTHER_KINDS:
+        raise ValueError(f"kind must be one of {sorted(SMOOTHER_KINDS)}")
     build_hierarchy(dim, degree, finest_level)  # same argument validation
     lib = _lib.load()
     h = ctypes.c_void_p()
-    check(lib.pmg_mg_create(dim, degree, finest_level, _dtype_code(dtype), _variant_code(variant),
-                            device, ctypes.byref(h)), "make_multigrid_context")
-    return MultigridContext(h.value, dim, degree, finest_level, variant, dtype, device)
+    check(lib.pmg_mg_create_kind(dim, degree, finest_level, _dtype_code(dtype), _variant_code(variant),
+                                 SMOOTHER_KINDS[kind], device, ctypes.byref(h)), "make_multigrid_context")
+    ctx = MultigridContext(h.value, dim, degree, finest_level, variant, dtype, device)
+    ctx.kind = kind
+    return ctx
+
+
+def point_gauss_seidel(ctx: LevelContext, x, b) -> None:
+    """One forward lexicographic Gauss-Seidel sweep on the level's operator
+    (point_gauss_seidel(assemble_sparse(level), x, b), smoother.cpp:160-166),
+    f64, x in place."""
+    if ctx.dtype != np.float64:
+        raise ValueError("point Gauss-Seidel runs in f64 only")
+    n = ctx.level.total_dofs
+    xa = _Arr(x, n, PMG_F64, "x", True)
+    ba = _Arr(b, n, PMG_F64, "b", False)
+    lib = _lib.load()
+    if _same_kind(xa, ba):
+        check(lib.pmg_point_gauss_seidel(ctx.handle, xa.ptr, ba.ptr, _stream((xa, ba), ctx)), "point_gauss_seidel")
+    else:
+        check(lib.pmg_point_gauss_seidel_host(ctx.handle, ctypes.cast(xa.ptr, ctypes.POINTER(ctypes.c_double)),
+                                              ctypes.cast(ba.ptr, ctypes.POINTER(ctypes.c_double))),
+              "point_gauss_seidel")
+
+
+def assemble_sparse(level: CartesianLevel):
+    """CSR matrix of the level operator (operator.cpp:194-281), host:
+    (row_ptr int64[N+1], cols int32[nnz], vals float64[nnz])."""
+    lib = _lib.load()
+    nnz = ctypes.c_int64()
+    check(lib.pmg_assemble_sparse_host(level.dim, level.degree, level.level, None, None, None, ctypes.byref(nnz)),
+          "assemble_sparse")
+    rp = np.zeros(level.total_dofs + 1, dtype=np.int64)
+    cols = np.zeros(nnz.value, dtype=np.int32)
+    vals = np.zeros(nnz.value)
+    check(lib.pmg_assemble_sparse_host(level.dim, level.degree, level.level,
+                                       rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                       cols.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                       vals.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(nnz)),
+          "assemble_sparse")
+    return rp, cols, vals
 
 
 def v_cycle(ctx: MultigridContext, li: int, x, b, use_graph: bool = False) -> None:
@@ -694,6 +737,7 @@ class MultiGpuContext:
         m = (1 << finest_level) * degree - 1
         self.mz = stack * (1 << finest_level) * degree - 1
         self.total_dofs = m * m * self.mz
+        self._devices = list(devices) if devices is not None else None
         if _handle is not None:
             self._h = _handle
         else:
@@ -720,7 +764,7 @@ class MultiGpuContext:
         check(lib.pmg_dd_create_rank(world, rank, device, buf, dim, degree, finest_level, stack,
                                      _dtype_code(dtype), _variant_code(variant), ctypes.byref(h)),
               "MultiGpuContext.for_rank")
-        return cls(None, dim, degree, finest_level, stack, dtype, variant, _handle=h)
+        return cls([device], dim, degree, finest_level, stack, dtype, variant, _handle=h)
 
     def slab(self, local: int = 0, which: str = "x"):
         """(device pointer, first global plane, planes, own_lo, own_hi)."""
@@ -729,6 +773,24 @@ class MultiGpuContext:
         check(_lib.load().pmg_dd_slab(self._h, local, 0 if which == "x" else 1, ctypes.byref(p), ctypes.byref(z0),
                                       ctypes.byref(np_), ctypes.byref(lo), ctypes.byref(hi)), "dd_slab")
         return p.value, z0.value, np_.value, lo.value, hi.value
+
+    def slab_tensor(self, local: int = 0, which: str = "x"):
+        """The slab of local rank `local` as a torch CUDA tensor (no copy; the
+        memory stays owned by the context)."""
+        import torch
+
+        ptr, _, nplanes, _, _ = self.slab(local, which)
+        m = (1 << self.finest_level) * self.degree - 1
+        n = nplanes * m * m
+        _, rank = self.stream(local)
+        dev = self._devices[local] if self._devices else torch.cuda.current_device()
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8" if self.dtype == np.float64 else "<f4",
+                                        "data": (ptr, False), "version": 3, "strides": None}
+
+        with torch.cuda.device(dev):
+            return torch.as_tensor(_View(), device=f"cuda:{dev}")
 
     def stream(self, local: int = 0):
         """(cudaStream_t of local rank `local`, its global rank)."""

@@ -32,6 +32,9 @@ def lib():
             "ref_fill_uniform": (None, [ctypes.c_uint64, i64, vp, i64, vp]),
             "ref_mg_create": (vp, [i, i, i, i, i, i]),
             "ref_mg_destroy": (None, [vp]),
+            "ref_mg_create_kind": (vp, [i, i, i, i, i, i, i, pi]),
+            "ref_point_gs": (i, [vp, i, vp, vp]),
+            "ref_assemble_sparse": (i, [i, i, i, vp, vp, vp, ctypes.POINTER(ctypes.c_int64)]),
             "ref_mg_set_threads": (None, [vp, i]),
             "ref_mg_total_dofs": (i64, [vp, i]),
             "ref_smooth": (i, [vp, i, i, vp, vp]),
