@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -101,7 +102,18 @@ struct pmg_level_s
   DevBuf red;             // reduction partials + result (double)
   DevBuf io[3];           // staging for the *_host entry points
   cudaStream_t io_stream = nullptr;
+  cudaStream_t io_h2d = nullptr, io_d2h = nullptr;  // copy streams of the pipelined *_host smoother
+  std::vector<cudaEvent_t> io_ev;                    // its per-chunk events
   std::shared_ptr<GsData> gs;  // point Gauss-Seidel data (gs.cu), built on first use
+  ~pmg_level_s()
+  {
+    // the owner set the level's device (pmg_level_destroy / pmg_mg_destroy)
+    for (cudaStream_t st : {io_stream, io_h2d, io_d2h})
+      if (st)
+        cudaStreamDestroy(st);
+    for (cudaEvent_t e : io_ev)
+      cudaEventDestroy(e);
+  }
 };
 
 struct CachedGraph
@@ -796,6 +808,138 @@ T *shift(void *p, int64_t zoff, int64_t plane)
 }
 }  // namespace
 
+namespace
+{
+// ---- the *_host smoother as a copy / compute pipeline ----------------------
+// pmg_smooth_host moves 2 N words in and N out over PCIe for a step whose
+// kernels take a fraction of that time. The step runs as a skewed wavefront
+// over the patch-vertex planes of the slowest direction: at pipeline step t
+// colour c covers the vertex planes (B[t-1] - c, B[t] - c] (B[t] - B[t-1] per
+// step, shrinking towards the end). The colour-to-colour dependencies reach
+// one vertex plane, so colour c at step t sees colour c - 1 already applied on
+// its planes +- 1 (same step, earlier launch) and colour c + 1 not yet applied
+// (it trails by one plane):
+// every patch is computed exactly as in pmg_smooth, bitwise. x / b planes go
+// H2D on one stream just ahead of colour 0; the planes whose last writer
+// (colour 7 of vertex planes <= t w - 7) is done go D2H on another, so both
+// transfer directions and the kernels overlap.
+int host_pipeline_chunks(const pmg_level_s *l, int variant)
+{
+  static const int forced = [] {
+    const char *e = std::getenv("PMG_HOST_PIPELINE");  // 0: off, n: n steps of vertex planes
+    return e ? std::atoi(e) : -1;
+  }();
+  if (l->S.dim != 3 || !(variant == PMG_FUSED || variant == PMG_BOUNDARY) || forced == 0)
+    return 1;
+  const int nv = l->S.n - 1;
+  if (forced > 0)
+    return std::max(1, std::min(forced, nv / 2));
+  if (l->S.N < (int64_t(1) << 20))
+    return 1;  // launch latency would dominate the saved transfer time
+  return std::max(1, std::min(4, nv / 4));
+}
+
+template <typename T>
+void smooth_host_pipelined(pmg_level_s *l, int variant, T *hx, const T *hb, T *dx, T *db)
+{
+  const int nv = l->S.n - 1, k = l->S.k, ncol = 1 << l->S.dim;
+  // colour 0 reaches vertex plane B[t] at step t; colour ncol-1 trails by
+  // ncol-1 planes, so B[steps] = nv + ncol - 1. Steps shrink linearly: the
+  // work left after the last H2D chunk (its 2^d dependent launches and the
+  // D2H of the trailing planes) is the pipeline's tail.
+  const int steps = std::max(1, std::min(host_pipeline_chunks(l, variant), nv));
+  std::vector<int> B(steps + 1, 0);
+  {
+    const int64_t span = nv + ncol - 1, wsum = static_cast<int64_t>(steps) * (steps + 1) / 2;
+    int64_t acc = 0;
+    for (int t = 1; t <= steps; ++t)
+    {
+      acc += steps - t + 1;
+      B[t] = static_cast<int>((span * acc + wsum - 1) / wsum);
+    }
+    B[steps] = static_cast<int>(span);
+  }
+  const int64_t m = l->S.m, pl = m * m;
+  if (!l->io_h2d)
+    check_cuda(cudaStreamCreateWithFlags(&l->io_h2d, cudaStreamNonBlocking), "stream");
+  if (!l->io_d2h)
+    check_cuda(cudaStreamCreateWithFlags(&l->io_d2h, cudaStreamNonBlocking), "stream");
+  while (static_cast<int>(l->io_ev.size()) < 2 * steps + 1)
+  {
+    cudaEvent_t e;
+    check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    l->io_ev.push_back(e);
+  }
+  cudaEvent_t *ev_in = l->io_ev.data(), *ev_out = l->io_ev.data() + steps, ev_prev = l->io_ev[2 * steps];
+  // after everything earlier on the compute stream (previous users of dx / db)
+  check_cuda(cudaEventRecord(ev_prev, l->io_stream), "event");
+  check_cuda(cudaStreamWaitEvent(l->io_h2d, ev_prev, 0), "wait");
+  check_cuda(cudaStreamWaitEvent(l->io_d2h, ev_prev, 0), "wait");
+  int64_t in_done = 0, out_done = 0;  // dof planes [0, in_done) sent, [0, out_done) returned
+  // PMG_HOST_PIPELINE_TRACE=1: per-stream event timeline on stderr (diagnostics)
+  static const bool trace = std::getenv("PMG_HOST_PIPELINE_TRACE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> tr;
+  auto mark = [&](const std::string &name, cudaStream_t st) {
+    if (!trace)
+      return;
+    cudaEvent_t e;
+    check_cuda(cudaEventCreate(&e), "event");
+    check_cuda(cudaEventRecord(e, st), "event");
+    tr.push_back({name, e});
+  };
+  mark("start", l->io_h2d);
+  for (int t = 1; t <= steps; ++t)
+  {
+    // colour 0 at step t covers vertex planes up to B[t]: its closures read
+    // dof planes below k (B[t] + 1)
+    const int64_t need = std::min<int64_t>(m, static_cast<int64_t>(k) * (static_cast<int64_t>(B[t]) + 1));
+    if (need > in_done)
+    {
+      const size_t off = static_cast<size_t>(in_done * pl), cnt = static_cast<size_t>((need - in_done) * pl);
+      check_cuda(cudaMemcpyAsync(dx + off, hx + off, cnt * sizeof(T), cudaMemcpyHostToDevice, l->io_h2d), "H2D");
+      check_cuda(cudaMemcpyAsync(db + off, hb + off, cnt * sizeof(T), cudaMemcpyHostToDevice, l->io_h2d), "H2D");
+      in_done = need;
+      mark("h2d " + std::to_string(t), l->io_h2d);
+    }
+    check_cuda(cudaEventRecord(ev_in[t - 1], l->io_h2d), "event");
+    check_cuda(cudaStreamWaitEvent(l->io_stream, ev_in[t - 1], 0), "wait");
+    for (int color = 0; color < ncol; ++color)
+    {
+      const int hi = std::min(nv, B[t] - color), lo = std::max(1, B[t - 1] - color + 1);
+      if (lo <= hi)
+        smooth_color_slab_impl<T>(l, variant, color, dx, db, 0, l->S.n, lo, hi, l->io_stream);
+    }
+    mark("compute " + std::to_string(t), l->io_stream);
+    // planes whose writers (patches v with v <= p / k + 1) all finished colour
+    // ncol - 1: p < k V with V = B[t] - (ncol - 1)
+    const int V = B[t] - (ncol - 1);
+    const int64_t fin = t == steps ? m : std::min<int64_t>(m, static_cast<int64_t>(k) * std::max(0, V));
+    if (fin > out_done)
+    {
+      check_cuda(cudaEventRecord(ev_out[t - 1], l->io_stream), "event");
+      check_cuda(cudaStreamWaitEvent(l->io_d2h, ev_out[t - 1], 0), "wait");
+      const size_t off = static_cast<size_t>(out_done * pl), cnt = static_cast<size_t>((fin - out_done) * pl);
+      check_cuda(cudaMemcpyAsync(hx + off, dx + off, cnt * sizeof(T), cudaMemcpyDeviceToHost, l->io_d2h), "D2H");
+      out_done = fin;
+      mark("d2h " + std::to_string(t), l->io_d2h);
+    }
+  }
+  check_cuda(cudaStreamSynchronize(l->io_d2h), "sync");
+  if (trace)
+  {
+    check_cuda(cudaDeviceSynchronize(), "sync");
+    for (size_t i = 1; i < tr.size(); ++i)
+    {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tr[0].second, tr[i].second);
+      std::fprintf(stderr, "  %-12s %8.3f ms\n", tr[i].first.c_str(), ms);
+    }
+    for (auto &e : tr)
+      cudaEventDestroy(e.second);
+  }
+}
+}  // namespace
+
 extern "C" {
 
 const char *pmg_last_error(void) { return g_last_error.c_str(); }
@@ -842,8 +986,6 @@ int pmg_level_destroy(pmg_level h)
     if (h)
     {
       DeviceGuard dg(h->device);
-      if (h->io_stream)
-        cudaStreamDestroy(h->io_stream);
       delete h;
     }
   });
@@ -973,6 +1115,12 @@ int pmg_smooth_host(pmg_level h, int variant, void *x, const void *b)
     HostIO io(h);
     const size_t bytes = static_cast<size_t>(h->S.N) * h->tsize;
     void *dx = io.dev(0, bytes), *db = io.dev(1, bytes);
+    if (host_pipeline_chunks(h, variant) > 1)
+    {
+      PMG_DISPATCH_T(h, smooth_host_pipelined<T>(h, variant, static_cast<T *>(x), static_cast<const T *>(b),
+                                                 static_cast<T *>(dx), static_cast<T *>(db)));
+      return;
+    }
     io.h2d(dx, x, bytes);
     io.h2d(db, b, bytes);
     PMG_DISPATCH_T(h, smooth_impl<T>(h, variant, static_cast<T *>(dx), static_cast<const T *>(db),
@@ -1260,12 +1408,6 @@ int pmg_mg_destroy(pmg_mg h)
     if (h)
     {
       DeviceGuard dg(h->device);
-      for (auto *l : h->levels)
-        if (l->io_stream)
-        {
-          cudaStreamDestroy(l->io_stream);
-          l->io_stream = nullptr;
-        }
       delete h;
     }
   });

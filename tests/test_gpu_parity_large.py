@@ -145,3 +145,26 @@ def test_vcycle_f32_residual_criterion(pmg, cuda, case):
         r_want = ref64.residual(L - 1, want.astype(np.float64), b64)
         err = np.linalg.norm(r_got - r_want) / np.linalg.norm(b64)
         assert err < 1e-5, (use_graph, err)
+
+
+@pytest.mark.parametrize("k,L,dtype,variant", [(2, 6, np.float64, "fused"), (2, 6, np.float32, "boundary"),
+                                               (1, 7, np.float64, "fused"), (3, 6, np.float32, "fused"),
+                                               (4, 5, np.float64, "fused")])
+def test_host_smoother_pipeline_bitwise(cuda, k, L, dtype, variant):
+    """pmg_smooth_host runs as an H2D / colour-chunk / D2H pipeline on levels
+    of >= 2^20 DoF (capi.cu smooth_host_pipelined): bitwise the device step."""
+    import paper_2405_19004_b200 as pmg
+
+    lev = pmg.make_level_context(pmg.build_hierarchy(3, k, L)[-1], dtype=dtype)
+    n = lev.level.total_dofs
+    assert n >= 1 << 20
+    rng = np.random.default_rng(17)
+    x0, b = rng.uniform(-1, 1, n).astype(dtype), rng.uniform(-1, 1, n).astype(dtype)
+    xd = cuda.from_numpy(x0.copy()).cuda()
+    pmg.smooth(lev, xd, cuda.from_numpy(b).cuda(), variant)
+    xh = x0.copy()
+    pmg.smooth(lev, xh, b, variant)
+    assert np.array_equal(xh, xd.cpu().numpy())
+    pmg.smooth(lev, xh, b, variant)  # a second step through the same buffers / events
+    pmg.smooth(lev, xd, cuda.from_numpy(b).cuda(), variant)
+    assert np.array_equal(xh, xd.cpu().numpy())
