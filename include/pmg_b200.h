@@ -159,6 +159,14 @@ int pmg_full_multigrid(pmg_mg h, const void *const *rhs_per_level, void *x, doub
                        int max_iterations, int *iterations, double *history, int history_cap,
                        void *stream);
 
+/* Host-vector forms (the reference's std::span calls): rhs_host[li] and x
+ * are host arrays; x receives the solution. */
+int pmg_full_multigrid_host(pmg_mg h, const double *const *rhs_host, double *x, double tol,
+                            int max_iterations, int *iterations, double *history,
+                            int history_cap);
+/* ~ vector_norm(v)   multigrid.hpp:89 on a host vector (reduced on the device). */
+int pmg_vector_norm_host(const void *v, int64_t n, int dtype, int device, double *out);
+
 /* ~ compute_rhs(level, f)   operator.hpp:58-59, for f = 1 (kind 0) and
  *   f = d pi^2 prod sin(pi x_a) (kind 1); host output in f64. */
 int pmg_compute_rhs_host(int dim, int degree, int level, int kind, double *out);
@@ -187,6 +195,19 @@ int pmg_point_gauss_seidel_host(pmg_level h, double *x, const double *b);
 int pmg_assemble_sparse_host(int dim, int degree, int level, int64_t *row_ptr, int32_t *cols,
                              double *vals, int64_t *nnz);
 
+/* General fields (compute_rhs / l2_error with any ScalarField,
+ * operator.hpp:55-64): the caller evaluates f (or u_exact) at the reference's
+ * quadrature points — (k+2)^d Gauss points per cell, pmg_quadrature_rule
+ * gives the k+2 points / weights on [0,1] — into a DEVICE array
+ * fq[cell * (k+2)^d + q] (cells and q lexicographic, direction 0 fastest;
+ * the point of (cell c, q) is x_a = (c_a + xi_{q_a}) h, h = 2^-level), f64.
+ * pmg_compute_rhs_q: b (device, the level's dtype) = the reference's b_i =
+ * sum over cells of (w f) against phi_i; pmg_l2_error_q: ||u_h - u||_L2 with
+ * the same rule (synchronises `stream`). */
+int pmg_quadrature_rule(int degree, double *points, double *weights);
+int pmg_compute_rhs_q(pmg_level h, const double *fq, void *b, void *stream);
+int pmg_l2_error_q(pmg_level h, const void *x, const double *uq, double *out, void *stream);
+
 /* ---- mixed precision / Krylov (krylov.hpp:30-39) -------------------------
  * Right-preconditioned GMRES(restart) in f64 on the device with the V-cycle
  * of `prec` (an f32 context: mixed precision; an f64 context: double) as the
@@ -194,6 +215,11 @@ int pmg_assemble_sparse_host(int dim, int degree, int level, int64_t *row_ptr, i
 int pmg_gmres(pmg_mg op, pmg_mg prec, const void *b, void *x, double tol, int restart,
               int max_iterations, int *iterations, double *history, int history_cap,
               void *stream);
+
+/* ~ gmres(apply_A, apply_P, b, x, tol, restart, max_iterations)   krylov.hpp:30-39
+ *   with host vectors b, x (x: initial guess in, solution out). */
+int pmg_gmres_host(pmg_mg op, pmg_mg prec, const double *b, double *x, double tol, int restart,
+                   int max_iterations, int *iterations, double *history, int history_cap);
 
 /* ---- raw kernels (tests / bench) ----------------------------------------- */
 /* Setup data of a level as uploaded (f64 copies), for parity tests:

@@ -96,6 +96,12 @@ double f_sin(std::span<const double> p)
     v *= std::sin(std::numbers::pi * c);
   return v;
 }
+// a non-separable field for the general-ScalarField tests (kind 2)
+double f_gen(std::span<const double> p)
+{
+  const double z = p.size() > 2 ? p[2] : 0.25;
+  return std::exp(p[0] - 0.5 * p[1]) * (1.0 + p[1] * p[1]) * std::cos(2.0 * p[0] * z + p[1]);
+}
 double u_sin(std::span<const double> p)
 {
   double v = 1.0;
@@ -367,8 +373,20 @@ int ref_compute_rhs(int dim, int k, int level, int rhs, double *out)
 {
   return guard([&] {
     auto levels = build_hierarchy(dim, k, level);
-    auto b = compute_rhs(levels.back(), rhs == 0 ? ScalarField(f_one) : ScalarField(f_sin));
+    auto b = compute_rhs(levels.back(), rhs == 0   ? ScalarField(f_one)
+                                        : rhs == 1 ? ScalarField(f_sin)
+                                                   : ScalarField(f_gen));
     std::memcpy(out, b.data(), b.size() * sizeof(double));
+  });
+}
+
+// l2_error against the non-separable field f_gen (as an "exact solution")
+int ref_l2_error_gen(int dim, int k, int level, const double *x, double *out)
+{
+  return guard([&] {
+    auto levels = build_hierarchy(dim, k, level);
+    const auto &lev = levels.back();
+    *out = l2_error(lev, csp<double>(x, lev.total_dofs), ScalarField(f_gen));
   });
 }
 

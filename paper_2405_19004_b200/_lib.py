@@ -65,6 +65,12 @@ SIGNATURES = [
     ("pmg_l2_error_sin", _i, [_vp, _vp, _pd, _vp]),
     ("pmg_get_smoother_impl", _i, []),
     ("pmg_smoother_kernel", _i, [_vp, _i, _i, _pi]),
+    ("pmg_full_multigrid_host", _i, [_vp, ctypes.POINTER(_vp), _pd, _d, _i, _pi, _pd, _i]),
+    ("pmg_vector_norm_host", _i, [_vp, _i64, _i, _i, _pd]),
+    ("pmg_gmres_host", _i, [_vp, _vp, _pd, _pd, _d, _i, _i, _pi, _pd, _i]),
+    ("pmg_quadrature_rule", _i, [_i, _pd, _pd]),
+    ("pmg_compute_rhs_q", _i, [_vp, _vp, _vp, _vp]),
+    ("pmg_l2_error_q", _i, [_vp, _vp, _vp, _pd, _vp]),
     ("pmg_mg_create_kind", _i, [_i, _i, _i, _i, _i, _i, _i, ctypes.POINTER(_vp)]),
     ("pmg_point_gauss_seidel", _i, [_vp, _vp, _vp, _vp]),
     ("pmg_point_gauss_seidel_host", _i, [_vp, _pd, _pd]),

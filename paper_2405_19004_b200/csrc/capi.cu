@@ -1542,6 +1542,57 @@ int pmg_full_multigrid(pmg_mg h, const void *const *rhs, void *x, double tol, in
   });
 }
 
+int pmg_full_multigrid_host(pmg_mg h, const double *const *rhs_host, double *x, double tol, int max_iterations,
+                            int *iterations, double *history, int history_cap)
+{
+  std::vector<std::unique_ptr<DevBuf>> rhs;
+  std::vector<const void *> ptrs;
+  DevBuf dx;
+  int st = guard([&] {
+    if (!h || !rhs_host || !x)
+      throw InvalidArg("full_multigrid: null pointer");
+    DeviceGuard dg(h->device);
+    for (size_t li = 0; li < h->levels.size(); ++li)
+    {
+      if (!rhs_host[li])
+        throw InvalidArg("full_multigrid: need one rhs per level");
+      const size_t bytes = static_cast<size_t>(h->levels[li]->S.N) * sizeof(double);
+      rhs.push_back(std::make_unique<DevBuf>());
+      rhs.back()->ensure(bytes);
+      check_cuda(cudaMemcpy(rhs.back()->p, rhs_host[li], bytes, cudaMemcpyHostToDevice), "H2D");
+      ptrs.push_back(rhs.back()->p);
+    }
+    dx.ensure(static_cast<size_t>(h->levels.back()->S.N) * sizeof(double));
+  });
+  if (st != PMG_OK)
+    return st;
+  st = pmg_full_multigrid(h, ptrs.data(), dx.p, tol, max_iterations, iterations, history, history_cap, nullptr);
+  const int st2 = guard([&] {
+    DeviceGuard dg(h->device);
+    check_cuda(cudaDeviceSynchronize(), "sync");
+    check_cuda(cudaMemcpy(x, dx.p, dx.bytes, cudaMemcpyDeviceToHost), "D2H");
+  });
+  return st != PMG_OK ? st : st2;
+}
+
+int pmg_vector_norm_host(const void *v, int64_t n, int dtype, int device, double *out)
+{
+  DevBuf dv;
+  const int st = guard([&] {
+    if (!out || (n > 0 && !v) || n < 0)
+      throw InvalidArg("vector_norm: invalid arguments");
+    if (dtype != PMG_F64 && dtype != PMG_F32)
+      throw InvalidArg("vector_norm: bad dtype");
+    DeviceGuard dg(device);
+    const size_t bytes = static_cast<size_t>(n) * (dtype == PMG_F64 ? 8 : 4);
+    dv.ensure(bytes + 8);
+    check_cuda(cudaMemcpy(dv.p, v, bytes, cudaMemcpyHostToDevice), "H2D");
+  });
+  if (st != PMG_OK)
+    return st;
+  return pmg_norm2(dv.p, n, dtype, device, out, nullptr);
+}
+
 int pmg_compute_rhs_host(int dim, int degree, int level, int kind, double *out)
 {
   return guard([&] {

@@ -277,3 +277,286 @@ extern "C" int pmg_l2_error_sin(pmg_level h, const void *x, double *out, void *s
     *out = std::sqrt(sum);
   });
 }
+
+// ---------------------------------------------------------------------------
+// General fields (compute_rhs / l2_error with an arbitrary ScalarField,
+// operator.cpp:283-411). The field arrives as its values at the reference's
+// quadrature points, evaluated by the caller wherever f lives (a host
+// std::function in the C++ shim, a torch expression on the device in Python):
+//   fq[cell * Q + q], cells lexicographic (direction 0 fastest), Q = (k+2)^d
+//   Gauss points per cell, q lexicographic (direction 0 fastest); the point
+//   of (cell c, q) is x_a = (c_a + xi_{q_a}) h with xi = pmg_quadrature_rule.
+// rhs: C[cell][t] = sum_q w_q |K| f_q prod_a shape[q_a][t_a] (thread per
+// (cell, t); the threads of a cell read the same fq, broadcast from L1),
+// then b_i = sum over the <= 2^d cells containing node i (thread per node,
+// fixed order: deterministic, no atomics).
+// l2: thread per (cell, q): u_h(x_q) from the cell's nodal values, w (u_h -
+// u_q)^2, per-CTA partial sums added on the host in a fixed order.
+// ---------------------------------------------------------------------------
+namespace pmgb
+{
+namespace
+{
+
+template <int D>
+__global__ void __launch_bounds__(256) rhs_cell_kernel(const __grid_constant__ QuadData Q, int k, int n,
+                                                       const double *__restrict__ fq, double *__restrict__ C)
+{
+  pdl_prologue();
+  const int NP = k + 1, NQ = k + 2;
+  const int nt = D == 3 ? NP * NP * NP : NP * NP;
+  const int nq = D == 3 ? NQ * NQ * NQ : NQ * NQ;
+  const int64_t ncell = D == 3 ? static_cast<int64_t>(n) * n * n : static_cast<int64_t>(n) * n;
+  const double h = 1.0 / n, jac = D == 3 ? h * h * h : h * h;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < ncell * nt;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+  {
+    const int64_t cell = e / nt;
+    const int t = static_cast<int>(e - cell * nt);
+    const int t0 = t % NP, t1 = (t / NP) % NP, t2 = D == 3 ? t / (NP * NP) : 0;
+    const double *f = fq + cell * nq;
+    double acc = 0.0;
+    for (int q2 = 0; q2 < (D == 3 ? NQ : 1); ++q2)
+    {
+      const double s2 = D == 3 ? Q.w[q2] * Q.shape[q2][t2] : 1.0;
+      for (int q1 = 0; q1 < NQ; ++q1)
+      {
+        const double s12 = s2 * Q.w[q1] * Q.shape[q1][t1];
+        double row = 0.0;
+        for (int q0 = 0; q0 < NQ; ++q0)
+          row = fma(Q.w[q0] * Q.shape[q0][t0], __ldg(f + (q2 * NQ + q1) * NQ + q0), row);
+        acc = fma(s12, row, acc);
+      }
+    }
+    C[e] = jac * acc;
+  }
+}
+
+template <int D, typename T>
+__global__ void __launch_bounds__(256) rhs_gather_kernel(int k, int n, int64_t m, const double *__restrict__ C,
+                                                         T *__restrict__ b)
+{
+  pdl_prologue();
+  const int NP = k + 1;
+  const int nt = D == 3 ? NP * NP * NP : NP * NP;
+  const int64_t N = D == 3 ? m * m * m : m * m;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+  {
+    const int64_t g[3] = {i % m, (i / m) % m, D == 3 ? i / (m * m) : 0};
+    // per direction: the cells containing lattice node p = g + 1 and its local index
+    int nc[3] = {1, 1, 1}, cc[3][2] = {{0, 0}, {0, 0}, {0, 0}}, tt[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+    for (int a = 0; a < D; ++a)
+    {
+      const int64_t p = g[a] + 1;
+      if (p % k == 0)
+      {
+        nc[a] = 2;
+        cc[a][0] = static_cast<int>(p / k) - 1;
+        tt[a][0] = k;
+        cc[a][1] = static_cast<int>(p / k);
+        tt[a][1] = 0;
+      }
+      else
+      {
+        cc[a][0] = static_cast<int>(p / k);
+        tt[a][0] = static_cast<int>(p % k);
+      }
+    }
+    double s = 0.0;
+    for (int j2 = 0; j2 < (D == 3 ? nc[2] : 1); ++j2)
+      for (int j1 = 0; j1 < nc[1]; ++j1)
+        for (int j0 = 0; j0 < nc[0]; ++j0)
+        {
+          const int64_t cell = (D == 3 ? static_cast<int64_t>(cc[2][j2]) * n * n : 0) +
+                               static_cast<int64_t>(cc[1][j1]) * n + cc[0][j0];
+          const int t = ((D == 3 ? tt[2][j2] : 0) * NP + tt[1][j1]) * NP + tt[0][j0];
+          s += C[cell * nt + t];
+        }
+    b[i] = static_cast<T>(s);
+  }
+}
+
+template <int D, typename T>
+__global__ void __launch_bounds__(256) l2err_q_kernel(const __grid_constant__ QuadData Q, int k, int n, int64_t m,
+                                                      const T *__restrict__ x, const double *__restrict__ uq,
+                                                      double *__restrict__ partial)
+{
+  pdl_prologue();
+  __shared__ double red[256];
+  const int NP = k + 1, NQ = k + 2;
+  const int nq = D == 3 ? NQ * NQ * NQ : NQ * NQ;
+  const int64_t ncell = D == 3 ? static_cast<int64_t>(n) * n * n : static_cast<int64_t>(n) * n;
+  const double h = 1.0 / n, jac = D == 3 ? h * h * h : h * h;
+  double acc = 0.0;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < ncell * nq;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+  {
+    const int64_t cell = e / nq;
+    const int q = static_cast<int>(e - cell * nq);
+    const int q0 = q % NQ, q1 = (q / NQ) % NQ, q2 = D == 3 ? q / (NQ * NQ) : 0;
+    const int c0 = static_cast<int>(cell % n), c1 = static_cast<int>((cell / n) % n),
+              c2 = D == 3 ? static_cast<int>(cell / (static_cast<int64_t>(n) * n)) : 0;
+    double uh = 0.0;
+    for (int t2 = 0; t2 < (D == 3 ? NP : 1); ++t2)
+    {
+      const int64_t g2 = static_cast<int64_t>(k) * c2 + t2;
+      if (D == 3 && (g2 < 1 || g2 > m))
+        continue;
+      const double s2 = D == 3 ? Q.shape[q2][t2] : 1.0;
+      for (int t1 = 0; t1 < NP; ++t1)
+      {
+        const int64_t g1 = static_cast<int64_t>(k) * c1 + t1;
+        if (g1 < 1 || g1 > m)
+          continue;
+        double row = 0.0;
+        for (int t0 = 0; t0 < NP; ++t0)
+        {
+          const int64_t g0 = static_cast<int64_t>(k) * c0 + t0;
+          if (g0 < 1 || g0 > m)
+            continue;
+          row = fma(Q.shape[q0][t0], static_cast<double>(x[((D == 3 ? (g2 - 1) * m : 0) + (g1 - 1)) * m + (g0 - 1)]),
+                    row);
+        }
+        uh = fma(s2 * Q.shape[q1][t1], row, uh);
+      }
+    }
+    const double err = uh - uq[e];
+    const double w = jac * Q.w[q0] * Q.w[q1] * (D == 3 ? Q.w[q2] : 1.0);
+    acc = fma(w, err * err, acc);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1)
+  {
+    if (threadIdx.x < st)
+      red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    partial[blockIdx.x] = red[0];
+}
+
+QuadData quad_data(int k)
+{
+  QuadData Q{};
+  const auto nodes = lobatto_nodes(k);
+  std::vector<double> qx, qw;
+  gauss_rule(k + 2, qx, qw);
+  for (int q = 0; q < k + 2; ++q)
+  {
+    Q.w[q] = qw[q];
+    Q.x[q] = qx[q];
+    const auto v = lagrange_eval(nodes, qx[q]);
+    for (int t = 0; t <= k; ++t)
+      Q.shape[q][t] = v[t];
+  }
+  return Q;
+}
+
+}  // namespace
+}  // namespace pmgb
+
+extern "C" int pmg_quadrature_rule(int degree, double *points, double *weights)
+{
+  return capi_guard([&] {
+    if (degree < 1 || degree > 7 || !points || !weights)
+      throw std::invalid_argument("quadrature_rule: invalid arguments");
+    const QuadData Q = quad_data(degree);
+    for (int q = 0; q < degree + 2; ++q)
+    {
+      points[q] = Q.x[q];
+      weights[q] = Q.w[q];
+    }
+  });
+}
+
+extern "C" int pmg_compute_rhs_q(pmg_level h, const double *fq, void *b, void *stream)
+{
+  return capi_guard([&] {
+    if (!h || !fq || !b)
+      throw std::invalid_argument("compute_rhs: null argument");
+    int dim = 0, k = 0, level = 0, dtype = 0, device = 0;
+    level_params(h, &dim, &k, &level, &dtype, &device);
+    DevScope dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const QuadData Q = quad_data(k);
+    const int n = 1 << level;
+    const int64_t m = static_cast<int64_t>(n) * k - 1;
+    const int64_t ncell = dim == 3 ? static_cast<int64_t>(n) * n * n : static_cast<int64_t>(n) * n;
+    const int64_t nt = dim == 3 ? static_cast<int64_t>(k + 1) * (k + 1) * (k + 1) : static_cast<int64_t>(k + 1) * (k + 1);
+    double *C = nullptr;
+    check_cuda(cudaMallocAsync(&C, static_cast<size_t>(ncell * nt) * sizeof(double), s), "compute_rhs alloc");
+    const int grid = level_sm_count(h) * 16;
+    if (dim == 3)
+      pdl_launch(rhs_cell_kernel<3>, dim3(grid), dim3(256), 0, s, Q, k, n, fq, C);
+    else
+      pdl_launch(rhs_cell_kernel<2>, dim3(grid), dim3(256), 0, s, Q, k, n, fq, C);
+    check_launch("rhs_cell_kernel");
+    if (dtype == PMG_F64)
+    {
+      if (dim == 3)
+        pdl_launch(rhs_gather_kernel<3, double>, dim3(grid), dim3(256), 0, s, k, n, m, static_cast<const double *>(C),
+                   static_cast<double *>(b));
+      else
+        pdl_launch(rhs_gather_kernel<2, double>, dim3(grid), dim3(256), 0, s, k, n, m, static_cast<const double *>(C),
+                   static_cast<double *>(b));
+    }
+    else
+    {
+      if (dim == 3)
+        pdl_launch(rhs_gather_kernel<3, float>, dim3(grid), dim3(256), 0, s, k, n, m, static_cast<const double *>(C),
+                   static_cast<float *>(b));
+      else
+        pdl_launch(rhs_gather_kernel<2, float>, dim3(grid), dim3(256), 0, s, k, n, m, static_cast<const double *>(C),
+                   static_cast<float *>(b));
+    }
+    check_launch("rhs_gather_kernel");
+    check_cuda(cudaFreeAsync(C, s), "compute_rhs free");
+  });
+}
+
+extern "C" int pmg_l2_error_q(pmg_level h, const void *x, const double *uq, double *out, void *stream)
+{
+  return capi_guard([&] {
+    if (!h || !x || !uq || !out)
+      throw std::invalid_argument("l2_error: null argument");
+    int dim = 0, k = 0, level = 0, dtype = 0, device = 0;
+    level_params(h, &dim, &k, &level, &dtype, &device);
+    DevScope dg(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const QuadData Q = quad_data(k);
+    const int n = 1 << level;
+    const int64_t m = static_cast<int64_t>(n) * k - 1;
+    const int grid = level_sm_count(h) * 8;
+    double *partial = nullptr;
+    check_cuda(cudaMallocAsync(&partial, grid * sizeof(double), s), "l2_error alloc");
+    if (dtype == PMG_F64)
+    {
+      if (dim == 3)
+        pdl_launch(l2err_q_kernel<3, double>, dim3(grid), dim3(256), 0, s, Q, k, n, m, static_cast<const double *>(x),
+                   uq, partial);
+      else
+        pdl_launch(l2err_q_kernel<2, double>, dim3(grid), dim3(256), 0, s, Q, k, n, m, static_cast<const double *>(x),
+                   uq, partial);
+    }
+    else
+    {
+      if (dim == 3)
+        pdl_launch(l2err_q_kernel<3, float>, dim3(grid), dim3(256), 0, s, Q, k, n, m, static_cast<const float *>(x), uq,
+                   partial);
+      else
+        pdl_launch(l2err_q_kernel<2, float>, dim3(grid), dim3(256), 0, s, Q, k, n, m, static_cast<const float *>(x), uq,
+                   partial);
+    }
+    check_launch("l2err_q_kernel");
+    std::vector<double> hp(grid);
+    check_cuda(cudaMemcpyAsync(hp.data(), partial, grid * sizeof(double), cudaMemcpyDeviceToHost, s), "l2_error D2H");
+    check_cuda(cudaFreeAsync(partial, s), "l2_error free");
+    check_cuda(cudaStreamSynchronize(s), "l2_error sync");
+    double sum = 0.0;
+    for (double v : hp)
+      sum += v;
+    *out = std::sqrt(sum);
+  });
+}

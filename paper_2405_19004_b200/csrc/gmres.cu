@@ -204,3 +204,30 @@ extern "C" int pmg_gmres(pmg_mg op, pmg_mg prec, const void *b_, void *x_, doubl
     flush_hist();
   });
 }
+
+// ---- host-vector entry points (the reference's std::span convention) -------
+extern "C" int pmg_gmres_host(pmg_mg op, pmg_mg prec, const double *b, double *x, double tol, int restart,
+                              int max_iterations, int *iterations, double *history, int history_cap)
+{
+  using namespace pmgb;
+  DevBuf db, dx;
+  int st = capi_guard([&] {
+    if (!op || !b || !x)
+      throw std::invalid_argument("gmres: invalid arguments");
+    DevScope dg(mg_device(op));
+    const size_t bytes = static_cast<size_t>(level_total(mg_level_ptr(op, mg_levels(op) - 1))) * sizeof(double);
+    db.ensure(bytes);
+    dx.ensure(bytes);
+    check_cuda(cudaMemcpy(db.p, b, bytes, cudaMemcpyHostToDevice), "H2D");
+    check_cuda(cudaMemcpy(dx.p, x, bytes, cudaMemcpyHostToDevice), "H2D");
+  });
+  if (st != PMG_OK)
+    return st;
+  st = pmg_gmres(op, prec, db.p, dx.p, tol, restart, max_iterations, iterations, history, history_cap, nullptr);
+  const int st2 = capi_guard([&] {
+    DevScope dg(mg_device(op));
+    check_cuda(cudaDeviceSynchronize(), "sync");
+    check_cuda(cudaMemcpy(x, dx.p, dx.bytes, cudaMemcpyDeviceToHost), "D2H");
+  });
+  return st != PMG_OK ? st : st2;
+}

@@ -38,7 +38,7 @@ __all__ = [
     "full_multigrid", "FmgStats", "vector_norm", "compute_rhs", "l2_error", "gmres", "SolveStats",
     "DivergenceError", "set_smoother_impl", "get_smoother_impl", "compute_rhs_device",
     "compute_residual_slab", "restrict_slab", "prolongate_slab", "smoother_kernel", "KERNEL_NAMES",
-    "MultiGpuContext", "nccl_unique_id", "point_gauss_seidel", "assemble_sparse", "SMOOTHER_KINDS",
+    "MultiGpuContext", "nccl_unique_id", "quadrature_points", "point_gauss_seidel", "assemble_sparse", "SMOOTHER_KINDS",
 ]
 
 _SMOOTHER_IMPLS = {"auto": 0, "line": 1, "plane": 2, "sweep": 3, "patch": 4}
@@ -617,35 +617,106 @@ def full_multigrid(ctx: MultigridContext, rhs_per_level, x, tol: float, max_iter
     return FmgStats(its.value, history)
 
 
-def compute_rhs(level: CartesianLevel, f: str = "one") -> np.ndarray:
-    """b_i = int f phi_i (operator.hpp:58-59) for f = 1 ('one') or
-    f = d pi^2 prod sin(pi x_a) ('sin')."""
-    kinds = {"one": 0, "sin": 1}
-    if f not in kinds:
-        raise ValueError("compute_rhs: f must be 'one' or 'sin'")
+def quadrature_points(level: CartesianLevel, device: int = 0):
+    """The reference's quadrature points of a level (operator.cpp:283-411:
+    (k+2)-point Gauss per direction and cell) as a float64 CUDA tensor of shape
+    (cells * (k+2)^d, d): cells lexicographic, direction 0 fastest, then the
+    points of a cell, direction 0 fastest (the fq layout of pmg_compute_rhs_q)."""
+    import torch
+
+    k, d, n = level.degree, level.dim, level.cells_per_dim
+    pts = np.zeros(k + 2)
+    wts = np.zeros(k + 2)
+    check(_lib.load().pmg_quadrature_rule(k, pts.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                          wts.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), "quadrature_rule")
+    dev = f"cuda:{device}"
+    xi = torch.from_numpy(pts).to(dev)
+    c = torch.arange(n, dtype=torch.float64, device=dev)
+    h = 1.0 / n
+    # axis a of the (cell_{d-1}, ..., cell_0, q_{d-1}, ..., q_0) grid
+    cells = torch.meshgrid(*([c] * d), indexing="ij")          # (c_{d-1}.., c_0) order below
+    qs = torch.meshgrid(*([xi] * d), indexing="ij")
+    coords = []
+    for a in range(d):
+        ca = cells[d - 1 - a].reshape(-1, 1)                     # cell coordinate of direction a
+        qa = qs[d - 1 - a].reshape(1, -1)
+        coords.append(((ca + qa) * h).reshape(-1))
+    return torch.stack(coords, dim=1)
+
+
+def _field_values(level: CartesianLevel, f, device: int):
+    """f at the level's quadrature points: f(pts) with pts a (P, d) float64
+    CUDA tensor -> P values (the torch form of ScalarField, operator.hpp:41)."""
+    import torch
+
+    pts = quadrature_points(level, device)
+    v = f(pts)
+    v = torch.as_tensor(v, dtype=torch.float64, device=pts.device).reshape(-1).contiguous()
+    if v.numel() != pts.shape[0]:
+        raise ValueError("field must return one value per quadrature point")
+    return v
+
+
+_KINDS = {"one": 0, "sin": 1}
+
+
+def compute_rhs(level: CartesianLevel, f="one") -> np.ndarray:
+    """b_i = int f phi_i (operator.hpp:58-59) as a host f64 array: f = 'one'
+    (f = 1), 'sin' (d pi^2 prod sin(pi x_a)), or any field f(pts) -> values
+    evaluated on the device at the reference's quadrature points and assembled
+    there (pmg_compute_rhs_q)."""
+    if callable(f):
+        import torch
+
+        ctx = make_level_context(level, np.float64, 0)
+        out = torch.zeros(level.total_dofs, dtype=torch.float64, device="cuda:0")
+        compute_rhs_device(ctx, f, out)
+        return out.cpu().numpy()
+    if f not in _KINDS:
+        raise ValueError("compute_rhs: f must be 'one', 'sin' or a callable field")
     out = np.zeros(level.total_dofs)
-    check(_lib.load().pmg_compute_rhs_host(level.dim, level.degree, level.level, kinds[f],
+    check(_lib.load().pmg_compute_rhs_host(level.dim, level.degree, level.level, _KINDS[f],
                                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), "compute_rhs")
     return out
 
 
-def compute_rhs_device(ctx: LevelContext, f: str, out) -> None:
+def compute_rhs_device(ctx: LevelContext, f, out) -> None:
     """compute_rhs on the device into `out` (a CUDA tensor of the level's
-    dtype): the tensor power of the 1D load vector, exact on the uniform
-    level (operator.cpp:283-344 computes the same integrals cell by cell)."""
-    kinds = {"one": 0, "sin": 1}
-    if f not in kinds:
-        raise ValueError("compute_rhs: f must be 'one' or 'sin'")
+    dtype). 'one' / 'sin': the tensor power of the 1D load vector, exact on
+    the uniform level; a callable field: its values at the quadrature points,
+    integrated cell by cell against the basis (operator.cpp:283-344)."""
     a = _Arr(out, ctx.level.total_dofs, ctx._code, "b", True)
-    check(_lib.load().pmg_compute_rhs(ctx.handle, kinds[f], a.ptr, _stream([out], ctx)), "compute_rhs")
+    if callable(f):
+        fq = _field_values(ctx.level, f, ctx.device)
+        check(_lib.load().pmg_compute_rhs_q(ctx.handle, ctypes.c_void_p(fq.data_ptr()), a.ptr,
+                                            _stream([out], ctx)), "compute_rhs")
+        return
+    if f not in _KINDS:
+        raise ValueError("compute_rhs: f must be 'one', 'sin' or a callable field")
+    check(_lib.load().pmg_compute_rhs(ctx.handle, _KINDS[f], a.ptr, _stream([out], ctx)), "compute_rhs")
 
 
-def l2_error(level, x, u_exact: str = "sin") -> float:
-    """L2 error against u = prod sin(pi x_a) (operator.hpp:62-64). With a
-    LevelContext and a CUDA tensor the (k+2)^d-point Gauss rule runs on the
-    device (pointwise, no cancellation); otherwise on the host."""
+def l2_error(level, x, u_exact="sin") -> float:
+    """L2 error ||u_h - u|| (operator.hpp:62-64) with the (k+2)^d-point Gauss
+    rule, u = prod sin(pi x_a) ('sin') or any field u(pts) -> values. With a
+    LevelContext and a CUDA tensor it runs on the device."""
+    if callable(u_exact):
+        import torch
+
+        if isinstance(level, LevelContext):
+            ctx = level
+        else:
+            ctx = make_level_context(level, np.float64, 0)
+        xd = x if (_is_torch(x) and x.is_cuda) else torch.from_numpy(
+            np.ascontiguousarray(x, dtype=ctx.dtype)).to(f"cuda:{ctx.device}")
+        a = _Arr(xd, ctx.level.total_dofs, ctx._code, "x", False)
+        uq = _field_values(ctx.level, u_exact, ctx.device)
+        out = ctypes.c_double()
+        check(_lib.load().pmg_l2_error_q(ctx.handle, a.ptr, ctypes.c_void_p(uq.data_ptr()), ctypes.byref(out),
+                                         _stream([xd], ctx)), "l2_error")
+        return out.value
     if u_exact != "sin":
-        raise ValueError("l2_error: only u = prod sin(pi x) is provided")
+        raise ValueError("l2_error: u_exact must be 'sin' or a callable field")
     if isinstance(level, LevelContext) and _is_torch(x) and x.is_cuda:
         a = _Arr(x, level.level.total_dofs, level._code, "x", False)
         out = ctypes.c_double()

@@ -45,6 +45,7 @@ def lib():
             "ref_vcycle": (i, [vp, i, vp, vp]),
             "ref_compute_rhs": (i, [i, i, i, i, vp]),
             "ref_l2_error_sin": (i, [i, i, i, vp, pd]),
+            "ref_l2_error_gen": (i, [i, i, i, vp, pd]),
             "ref_fmg": (i, [vp, i, d, i, vp, pi, vp, i]),
             "ref_gmres": (i, [vp, vp, i, vp, vp, d, i, i, pi, vp, i]),
             "ref_last_history_len": (i, []),

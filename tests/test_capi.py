@@ -160,7 +160,7 @@ def test_errors_mirror_reference(lib):
     with pytest.raises(ValueError):
         pmg.make_multigrid_context(3, 2, 0)
     with pytest.raises(ValueError):
-        pmg.make_multigrid_context(3, 2, 2, kind="point_gs")
+        pmg.make_multigrid_context(3, 2, 2, kind="bogus")
 
 
 def test_no_cpu_fallback_without_gpu(lib):
