@@ -496,20 +496,6 @@ def main():
     ridge = fp_peak * 1e12 / (hbm_peak * 1e9)  # flop/B
     binding = "roofline" if (not fits_l2 and step_flops / alg_bytes < ridge) else "roofline_fp"
 
-    # on-chip (shared-memory) roofline of the reference's contraction sequence
-    # (banksim.py, the paper's model) for the same flops
-    from paper_2405_19004_b200 import banksim
-
-    tm = banksim.shared_traffic_model(args.variant if args.variant in ("fused",) else "fused", args.degree,
-                                      args.dim, word)
-    hw = banksim.HardwareParams(sms=sm_count, clock_ghz=max_mhz / 1e3)
-    onchip_bound = banksim.onchip_roofline(tm.flops, tm.bytes_read, tm.bytes_written, hw)
-    roofline_onchip = {
-        "bound": "shared memory (reference contraction sequence)", "achieved": roofline_fp["achieved"],
-        "peak": onchip_bound, "unit": "TFLOP/s", "frac": roofline_fp["achieved"] / onchip_bound,
-        "model": "banksim.shared_traffic_model: per contraction |in| + n_out n_in reads, |out| writes",
-    }
-
     # ---- V-cycle throughput (secondary metric, single GPU) ---------------------
     vcycle = None
     if world == 1:
@@ -582,7 +568,6 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic (x, b ~ U(-1,1))", "config": cfg,
         "roofline": roofline, "roofline_fp": roofline_fp, "roofline_binding": binding,
-        "roofline_onchip": roofline_onchip,
         "e2e": {"value": N_total / t_e2e, "unit": "DoF/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "api": "pmg_smooth_host (C-ABI, pinned host buffers)" if world == 1 else
