@@ -276,7 +276,8 @@ def run_sweeps(args, pmg, torch, flush, stream, hbm_peak, max_mhz, sm_count):
     "fused vs straightforward" comparison (BASELINE configs[3]: 2D Q1..Q7
     ~2e8 DoF; plus 3D Q2 / Q4): naive = the reference's per-patch body moved
     to the GPU directly (csrc/naive.cu, one CTA per patch, global-memory
-    scratch)."""
+    scratch); global = the reference's global variant on the device (level
+    operator per colour into a global residual, then per-patch solves)."""
     K = args.sweep_steps
     common = (K, flush, stream, hbm_peak, max_mhz, sm_count)
     sweep = []
@@ -291,9 +292,13 @@ def run_sweeps(args, pmg, torch, flush, stream, hbm_peak, max_mhz, sm_count):
         if fused is None:
             fused = sweep_entry(pmg, torch, dim, k, L, "f64", "fused", *common)
         naive = sweep_entry(pmg, torch, dim, k, L, "f64", "naive", 2, *common[1:])
+        # the reference's own straightforward variant (smoother.cpp:63-81): the
+        # level operator over the whole level per colour, then the patch solves
+        glob = sweep_entry(pmg, torch, dim, k, L, "f64", "global", 2, *common[1:])
         comp.append({"dim": dim, "degree": k, "level": L, "dofs": fused["dofs"], "dtype": "f64",
                      "fused": fused["value"], "fused_kernel": fused["kernel"], "naive": naive["value"],
-                     "speedup": fused["value"] / naive["value"], "unit": "DoF/s"})
+                     "speedup": fused["value"] / naive["value"], "global": glob["value"],
+                     "speedup_vs_global": fused["value"] / glob["value"], "unit": "DoF/s"})
     return comp, sweep
 
 

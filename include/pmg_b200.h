@@ -328,6 +328,11 @@ int pmg_dd_residual_norm(pmg_dd h, double *out);
 int pmg_dd_full_multigrid(pmg_dd h, const double *const *rhs_host, double tol, int max_iterations,
                           int *iterations, double *history, int history_cap);
 int pmg_dd_synchronize(pmg_dd h);
+/* Host-only: the decomposition plan of one rank (owned vertex / dof planes,
+ * whether the level is split, the per-colour boundary-layer planes and plane
+ * messages), for tests and tools; see csrc/dd.cu. Returns the number of
+ * int64 written, or minus a pmg_status. */
+int64_t pmg_dd_plan(int world, int rank, int degree, int level, int stack, int64_t *out, int64_t cap);
 
 /* Number of kernel launches issued by this library since load (counter). */
 int64_t pmg_launch_count(void);

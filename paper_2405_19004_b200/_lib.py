@@ -90,6 +90,7 @@ SIGNATURES = [
     ("pmg_dd_residual_norm", _i, [_vp, _pd]),
     ("pmg_dd_full_multigrid", _i, [_vp, ctypes.POINTER(_vp), _d, _i, _pi, _pd, _i]),
     ("pmg_dd_synchronize", _i, [_vp]),
+    ("pmg_dd_plan", _i64, [_i, _i, _i, _i, _i, _pi64, _i64]),
 ]
 
 _lib = None

@@ -985,6 +985,45 @@ void check_vcycle(const pmg_dd_s *d, const char *what)
 
 extern "C" {
 
+// host-only view of the decomposition plan (tests compare it with dd.py):
+// out[0..6] = a, b, lo, hi, own_lo, own_hi, decomposed (this level is split
+// with a 2H halo); then per colour c: n_early, n_sends, n_recvs followed by
+// the early vertex planes and (peer, g0, np) per send / recv; returns the
+// number of int64 written (or PMG_ERR_INVALID via a negative count).
+int64_t pmg_dd_plan(int world, int rank, int degree, int level, int stack, int64_t *out, int64_t cap)
+{
+  int64_t n = -1;
+  const int st = dd_guard([&] {
+    if (!out || world < 1 || rank < 0 || rank >= world || degree < 1 || level < 1 || stack < 1)
+      throw InvalidArg("dd_plan: invalid arguments");
+    const Plan p = make_plan(world, rank, degree, level, stack);
+    std::vector<int64_t> v = {p.a, p.b, p.lo, p.hi, p.own_lo, p.own_hi};
+    const auto dl = stack == 1 ? decomposed_levels(world, degree, level) : std::vector<int>{};
+    v.push_back(std::find(dl.begin(), dl.end(), level) != dl.end() ? 1 : 0);
+    for (int c = 0; c < 8; ++c)
+    {
+      const ColourStep cs = colour_step(p, c);
+      v.push_back(static_cast<int64_t>(cs.early.size()));
+      v.push_back(static_cast<int64_t>(cs.sends.size()));
+      v.push_back(static_cast<int64_t>(cs.recvs.size()));
+      for (auto [lo, hi] : cs.early)
+        v.push_back(lo);
+      for (const auto *lst : {&cs.sends, &cs.recvs})
+        for (const Msg &m : *lst)
+        {
+          v.push_back(m.peer);
+          v.push_back(m.g0);
+          v.push_back(m.np);
+        }
+    }
+    if (static_cast<int64_t>(v.size()) > cap)
+      throw InvalidArg("dd_plan: output capacity too small");
+    std::copy(v.begin(), v.end(), out);
+    n = static_cast<int64_t>(v.size());
+  });
+  return st == PMG_OK ? n : -static_cast<int64_t>(st);
+}
+
 int pmg_dd_nccl_id(void *id_out)
 {
   return dd_guard([&] {

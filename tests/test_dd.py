@@ -246,3 +246,61 @@ def test_gloo_slab_vcycle(tmp_path, world, k, level):
     err, scale, agg = np.load(out)
     assert agg >= 1
     assert err <= 1e-13 * scale, (err, scale)
+
+
+# ---------------------------------------------------------------------------
+# The C++ decomposition (csrc/dd.cu, pmg_dd_*) follows the same plan as this
+# module: compare the host-only plan dump with make_plan / colour_step /
+# decomposed_levels over many (world, rank, k, level, stack). No GPU needed.
+# ---------------------------------------------------------------------------
+import ctypes  # noqa: E402
+
+
+def _cpp_plan(world, rank, k, level, stack):
+    from paper_2405_19004_b200 import _lib
+
+    buf = (ctypes.c_int64 * 4096)()
+    n = _lib.load().pmg_dd_plan(world, rank, k, level, stack, buf, 4096)
+    assert n > 0, n
+    v = list(buf[:n])
+    head, rest = v[:7], v[7:]
+    steps = []
+    for _ in range(8):
+        ne, ns, nr = rest[:3]
+        rest = rest[3:]
+        early = rest[:ne]
+        rest = rest[ne:]
+        sends = [tuple(rest[3 * i:3 * i + 3]) for i in range(ns)]
+        rest = rest[3 * ns:]
+        recvs = [tuple(rest[3 * i:3 * i + 3]) for i in range(nr)]
+        rest = rest[3 * nr:]
+        steps.append((early, sends, recvs))
+    return head, steps
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 7, 8])
+@pytest.mark.parametrize("k,level,stack", [(1, 4, 1), (2, 5, 1), (3, 4, 1), (4, 6, 1), (7, 3, 1), (2, 4, 4),
+                                           (3, 3, 8)])
+def test_cpp_plan_matches_python(world, k, level, stack):
+    from paper_2405_19004_b200 import dd
+
+    if (1 << level) * stack - 1 < world:
+        return
+    dl = dd.decomposed_levels(world, k, level) if stack == 1 else []
+    for rank in range(world):
+        p = dd.make_plan(world, rank, k, level, stack=stack)
+        head, steps = _cpp_plan(world, rank, k, level, stack)
+        assert head == [p.a, p.b, p.lo, p.hi, p.own_lo, p.own_hi, int(level in dl)]
+        for c in range(8):
+            st = dd.colour_step(p, c)
+            assert steps[c][0] == [lo for lo, _ in st.early]
+            assert steps[c][1] == [tuple(m) for m in st.sends]
+            assert steps[c][2] == [tuple(m) for m in st.recvs]
+
+
+def test_cpp_plan_errors():
+    from paper_2405_19004_b200 import _lib
+
+    buf = (ctypes.c_int64 * 16)()
+    assert _lib.load().pmg_dd_plan(8, 0, 2, 2, 1, buf, 16) < 0  # 3 vertex planes over 8 ranks
+    assert _lib.load().pmg_dd_plan(2, 0, 2, 5, 1, buf, 4) < 0   # capacity
