@@ -377,6 +377,10 @@ def main():
         dist.broadcast_object_list(nid, src=0)
         mctx = pmg.MultiGpuContext.for_rank(world, rank, local, nid[0], 3, args.degree, args.level, stack=world,
                                             dtype=dt, variant=args.variant)
+        # the step (8 colours: boundary layers, grouped NCCL plane messages,
+        # interiors) replayed as one captured CUDA graph
+        if os.environ.get("PMG_DD_GRAPH", "1") == "1":
+            mctx.set_graph(True)
         plan = dd.make_plan(world, rank, args.degree, args.level, stack=world)
         N_total = plan.m * plan.m * plan.mz
         x = mctx.slab_tensor(0, "x")
@@ -388,6 +392,12 @@ def main():
 
         def step():
             mctx.smooth()
+
+        graph_info = {"cuda_graph": os.environ.get("PMG_DD_GRAPH", "1") == "1"}
+        l0 = lib.pmg_launch_count()
+        step()  # the first call captures the graph: its launches are the step's
+        mctx.synchronize()
+        dd_step_launches = lib.pmg_launch_count() - l0
 
     else:
         # PMG_DD_SHARED_GPU: the Python driver (dd.py) over gloo, ranks sharing cuda:0
@@ -423,7 +433,11 @@ def main():
         step()
     barrier()
 
-    timed_step, graph_info, per_step_launches = step, None, None
+    timed_step, per_step_launches = step, None
+    if world == 1 or shared:
+        graph_info = None
+    elif graph_info["cuda_graph"]:
+        per_step_launches = dd_step_launches  # graph replays bypass the launch counter
 
     # ---- timed region: K steps, CUDA events per step, L2 flushed between ------
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]

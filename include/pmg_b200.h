@@ -316,8 +316,13 @@ int pmg_dd_stream(pmg_dd h, int local, void **stream, int *rank);
 int pmg_dd_scatter_host(pmg_dd h, int which, const void *global);
 int pmg_dd_gather_host(pmg_dd h, int which, void *global);
 int pmg_dd_set_smoothing(pmg_dd h, int pre_smooth, int post_smooth);
-/* One smoothing step of the finest level (x in place). */
+/* One smoothing step of the finest level (x in place). With
+ * pmg_dd_set_graph(h, 1) (all local ranks on one device: virtual ranks, or
+ * one process per GPU) the step is captured once as a CUDA graph (launches,
+ * events, plane copies / NCCL calls) and replayed on the first local rank's
+ * stream. */
 int pmg_dd_smooth(pmg_dd h);
+int pmg_dd_set_graph(pmg_dd h, int enable);
 /* One V-cycle from the finest level (x in place, b right-hand side). */
 int pmg_dd_v_cycle(pmg_dd h);
 /* ||b - A x|| of the finest level (all-reduced; synchronises). */

@@ -86,6 +86,7 @@ SIGNATURES = [
     ("pmg_dd_gather_host", _i, [_vp, _i, _vp]),
     ("pmg_dd_set_smoothing", _i, [_vp, _i, _i]),
     ("pmg_dd_smooth", _i, [_vp]),
+    ("pmg_dd_set_graph", _i, [_vp, _i]),
     ("pmg_dd_v_cycle", _i, [_vp]),
     ("pmg_dd_residual_norm", _i, [_vp, _pd]),
     ("pmg_dd_full_multigrid", _i, [_vp, ctypes.POINTER(_vp), _d, _i, _pi, _pd, _i]),

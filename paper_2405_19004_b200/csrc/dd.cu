@@ -325,9 +325,26 @@ struct pmg_dd_s
   std::vector<int> dd_levels;  // decomposed levels, finest first (empty: the V-cycle runs on rank 0)
   int agg = 0;                 // finest agglomerated mesh level
   std::vector<std::unique_ptr<Rank>> local;
+  bool use_graph = false;                 // pmg_dd_set_graph: smoothing step / V-cycle as CUDA graphs
+  bool capturing = false;                 // inside a capture: the coarse V-cycle runs eagerly (captured)
+  cudaGraphExec_t smooth_graph = nullptr, vcycle_graph = nullptr;
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> joins;
 
   ~pmg_dd_s()
   {
+    if (!local.empty())
+    {
+      cudaSetDevice(local[0]->device);
+      if (smooth_graph)
+        cudaGraphExecDestroy(smooth_graph);
+      if (vcycle_graph)
+        cudaGraphExecDestroy(vcycle_graph);
+      if (fork)
+        cudaEventDestroy(fork);
+      for (cudaEvent_t e : joins)
+        cudaEventDestroy(e);
+    }
     for (auto &r : local)
     {
       cudaSetDevice(r->device);
@@ -703,7 +720,8 @@ void vcycle_level(pmg_dd_s *d, int lev)
       DevScope g(root->device);
       // the recursion starts from x_c = 0 (multigrid.cpp:336)
       check_cuda(cudaMemsetAsync(root->L[lev].a[A_XC], 0, d->bytes(d->mz(cl) * d->ps(cl)), root->main), "x_c = 0");
-      ck(pmg_v_cycle(root->root_mg, cl - 1, root->L[lev].a[A_XC], root->L[lev].a[A_BC], 1, root->main),
+      ck(pmg_v_cycle(root->root_mg, cl - 1, root->L[lev].a[A_XC], root->L[lev].a[A_BC], d->capturing ? 0 : 1,
+                     root->main),
          "dd coarse V-cycle");
     }
     broadcast_from_root(d, lev, A_XC, d->mz(cl) * d->ps(cl));
@@ -752,7 +770,8 @@ void vcycle_agglomerated(pmg_dd_s *d)
   if (Rank *root = d->find(0))
   {
     DevScope g(root->device);
-    ck(pmg_v_cycle(root->root_mg, lev - 1, root->L[lev].a[A_XC], root->L[lev].a[A_BC], 1, root->main),
+    ck(pmg_v_cycle(root->root_mg, lev - 1, root->L[lev].a[A_XC], root->L[lev].a[A_BC], d->capturing ? 0 : 1,
+                   root->main),
        "dd V-cycle (agglomerated)");
   }
   broadcast_from_root(d, lev, A_XC, d->mz(lev) * ps);
@@ -982,6 +1001,83 @@ void check_vcycle(const pmg_dd_s *d, const char *what)
 }
 
 }  // namespace
+
+// one eager V-cycle with the finest x saved and restored: allocations of the
+// coarse single-device context (first use of its levels) happen outside a
+// capture
+static void vcycle_warm(pmg_dd_s *d)
+{
+  std::vector<DevBuf> save(d->local.size());
+  for (size_t i = 0; i < d->local.size(); ++i)
+  {
+    Rank &r = *d->local[i];
+    DevScope g(r.device);
+    LevelState &ls = r.L[d->finest];
+    const size_t bytes = d->bytes(ls.slab.np() * d->ps(d->finest));
+    save[i].ensure(bytes);
+    check_cuda(cudaMemcpyAsync(save[i].p, ls.a[A_X], bytes, cudaMemcpyDeviceToDevice, r.main), "save x");
+  }
+  vcycle_finest(d);
+  for (size_t i = 0; i < d->local.size(); ++i)
+  {
+    Rank &r = *d->local[i];
+    DevScope g(r.device);
+    LevelState &ls = r.L[d->finest];
+    check_cuda(cudaMemcpyAsync(ls.a[A_X], save[i].p, save[i].bytes, cudaMemcpyDeviceToDevice, r.main), "restore x");
+  }
+  sync_all(d);
+}
+
+static bool dd_graphable(const pmg_dd_s *d)
+{
+  for (auto &r : d->local)
+    if (r->device != d->local[0]->device)
+      return false;
+  return true;
+}
+
+template <typename F>
+static void dd_capture(pmg_dd_s *d, cudaGraphExec_t &exec, F &&body)
+{
+  Rank &r0 = *d->local[0];
+  DevScope g(r0.device);
+  if (!d->fork)
+    check_cuda(cudaEventCreateWithFlags(&d->fork, cudaEventDisableTiming), "event");
+  while (d->joins.size() < d->local.size())
+  {
+    cudaEvent_t e;
+    check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    d->joins.push_back(e);
+  }
+  sync_all(d);
+  cudaGraph_t graph = nullptr;
+  check_cuda(cudaStreamBeginCapture(r0.main, cudaStreamCaptureModeRelaxed), "capture begin");
+  try
+  {
+    check_cuda(cudaEventRecord(d->fork, r0.main), "event");
+    for (size_t i = 1; i < d->local.size(); ++i)
+      check_cuda(cudaStreamWaitEvent(d->local[i]->main, d->fork, 0), "wait");
+    d->capturing = true;
+    body();
+    d->capturing = false;
+    for (size_t i = 1; i < d->local.size(); ++i)
+    {
+      check_cuda(cudaEventRecord(d->joins[i], d->local[i]->main), "event");
+      check_cuda(cudaStreamWaitEvent(r0.main, d->joins[i], 0), "wait");
+    }
+  }
+  catch (...)
+  {
+    d->capturing = false;
+    cudaStreamEndCapture(r0.main, &graph);
+    if (graph)
+      cudaGraphDestroy(graph);
+    throw;
+  }
+  check_cuda(cudaStreamEndCapture(r0.main, &graph), "capture end");
+  check_cuda(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+  cudaGraphDestroy(graph);
+}
 
 extern "C" {
 
@@ -1216,11 +1312,46 @@ int pmg_dd_set_smoothing(pmg_dd h, int pre, int post)
   });
 }
 
+// the finest level's smoothing step captured once as one CUDA graph (all
+// local ranks on one device: virtual ranks, or one process per GPU): the
+// per-colour launches, events, copies / NCCL calls of smooth_level replay
+// without host work. The other ranks' streams fork from and join the first
+// rank's stream inside the capture.
+int pmg_dd_set_graph(pmg_dd h, int enable)
+{
+  return dd_guard([&] {
+    if (!h)
+      throw InvalidArg("null handle");
+    if (enable && !dd_graphable(h))
+      throw InvalidArg("dd_set_graph: the local ranks must share one device");
+    h->use_graph = enable != 0;
+    if (!h->use_graph)
+    {
+      DevScope g(h->local[0]->device);
+      sync_all(h);
+      for (cudaGraphExec_t *e : {&h->smooth_graph, &h->vcycle_graph})
+        if (*e)
+        {
+          cudaGraphExecDestroy(*e);
+          *e = nullptr;
+        }
+    }
+  });
+}
+
 int pmg_dd_smooth(pmg_dd h)
 {
   return dd_guard([&] {
     if (!h)
       throw InvalidArg("null handle");
+    if (h->use_graph)
+    {
+      if (!h->smooth_graph)
+        dd_capture(h, h->smooth_graph, [&] { smooth_level(h, h->finest); });
+      DevScope g(h->local[0]->device);
+      check_cuda(cudaGraphLaunch(h->smooth_graph, h->local[0]->main), "graph launch");
+      return;
+    }
     smooth_level(h, h->finest);
   });
 }
@@ -1231,6 +1362,19 @@ int pmg_dd_v_cycle(pmg_dd h)
     if (!h)
       throw InvalidArg("null handle");
     check_vcycle(h, "dd_v_cycle");
+    if (h->use_graph)
+    {
+      if (!h->vcycle_graph)
+      {
+        // the coarse context's workspaces are settled by one eager cycle
+        // first (a capture must not allocate): x is restored afterwards
+        vcycle_warm(h);
+        dd_capture(h, h->vcycle_graph, [&] { vcycle_finest(h); });
+      }
+      DevScope g(h->local[0]->device);
+      check_cuda(cudaGraphLaunch(h->vcycle_graph, h->local[0]->main), "graph launch");
+      return;
+    }
     vcycle_finest(h);
   });
 }

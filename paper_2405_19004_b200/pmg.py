@@ -890,6 +890,11 @@ class MultiGpuContext:
     def smooth(self) -> None:
         check(_lib.load().pmg_dd_smooth(self._h), "dd_smooth")
 
+    def set_graph(self, enable: bool = True) -> None:
+        """Replay the smoothing step as one captured CUDA graph (local ranks on
+        one device)."""
+        check(_lib.load().pmg_dd_set_graph(self._h, int(enable)), "dd_set_graph")
+
     def v_cycle(self) -> None:
         check(_lib.load().pmg_dd_v_cycle(self._h), "dd_v_cycle")
 

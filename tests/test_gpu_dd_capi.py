@@ -142,3 +142,35 @@ def test_dd_argument_errors(cuda):
         pmg.MultiGpuContext([0] * 8, 3, 2, 2)  # 3 vertex planes over 8 ranks
     with pytest.raises(ValueError):
         pmg.MultiGpuContext([0], 3, 2, 4, variant="global")
+
+
+@pytest.mark.parametrize("transport,P", [("copy", 3), ("copy", 1), ("nccl", 1)])
+def test_dd_smooth_graph_bitwise(cuda, transport, P):
+    """The captured smoothing step (pmg_dd_set_graph) replays bitwise the
+    eager one, repeatedly."""
+    import paper_2405_19004_b200 as pmg
+
+    k, L = 2, 6
+    eager = pmg.MultiGpuContext([0] * P, 3, k, L, transport=transport)
+    graph = pmg.MultiGpuContext([0] * P, 3, k, L, transport=transport)
+    graph.set_graph(True)
+    x0, b = _inputs(eager.total_dofs, np.float64, 21)
+    for c in (eager, graph):
+        c.scatter("x", x0)
+        c.scatter("b", b)
+        for _ in range(3):
+            c.smooth()
+        c.synchronize()
+    assert np.array_equal(eager.gather("x"), graph.gather("x"))
+    # the V-cycle as one graph (captured after one eager warm-up cycle that
+    # leaves x unchanged), twice in a row
+    for c in (eager, graph):
+        c.scatter("x", x0)
+        c.v_cycle()
+        c.v_cycle()
+        c.synchronize()
+    assert np.array_equal(eager.gather("x"), graph.gather("x"))
+    x1, _ = _single(k, L, np.float64, x0, b)[1], None
+    eager.scatter("x", x0)
+    eager.v_cycle()
+    assert np.array_equal(eager.gather("x"), x1)

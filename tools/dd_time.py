@@ -47,6 +47,10 @@ for P in (1, 2, 4, 8):
     ctx.scatter("b", bh)
     s = tm(ctx.smooth, ctx.synchronize)
     v = tm(ctx.v_cycle, ctx.synchronize)
+    ctx.set_graph(True)
+    sg = tm(ctx.smooth, ctx.synchronize)
+    vg = tm(ctx.v_cycle, ctx.synchronize)
     print(f"P={P} virtual ranks (decomposed levels {ctx.decomposed_levels}): smooth {s:.3f} ms "
-          f"({ts / s:.2f}x single), V-cycle {v:.3f} ms ({tv / v:.2f}x single)")
+          f"({ts / s:.2f}x single), as one graph {sg:.3f} ms ({ts / sg:.2f}x); V-cycle {v:.3f} ms "
+          f"({tv / v:.2f}x single), as one graph {vg:.3f} ms ({tv / vg:.2f}x)")
     del ctx
