@@ -80,9 +80,14 @@ static bool run_case(int device, int k, int L, int P, int dtype)
   {
     std::vector<T> r(N);
     CK(pmg_compute_residual_host(pmg_mg_level(mg, L - 1), xv.data(), b.data(), r.data()));
-    double s = 0;
+    double s = 0, comp = 0;  // compensated sum: 1e9 squares summed sequentially lose ~1e-11
     for (T e : r)
-      s += double(e) * double(e);
+    {
+      const double y = double(e) * double(e) - comp;
+      const double t = s + y;
+      comp = (t - s) - y;
+      s = t;
+    }
     rn1 = std::sqrt(s);
   }
   const double rn_rel = std::fabs(rn - rn1) / rn1;
