@@ -284,6 +284,10 @@ def run_sweeps(args, pmg, torch, flush, stream, hbm_peak, max_mhz, sm_count):
     for dtype in ("f64", "f32"):
         for k in range(1, 8):
             sweep.append(sweep_entry(pmg, torch, 3, k, C3_LEVELS[k], dtype, "fused", *common, vcycle=True))
+    # C5 (3D Q4, 2^8 cells per direction, 1.07e9 DoF, 8.6 GB per f64 vector):
+    # the multi-GPU configuration's whole problem on ONE B200 (the strong-
+    # scaling baseline; weak-scaling unit = the Q4 L7 entry above)
+    sweep.append(sweep_entry(pmg, torch, 3, 4, 8, "f64", "fused", *common, vcycle=True))
     comp = []
     cases = [(2, k, C4_LEVELS[k]) for k in range(1, 8)] + [(3, 2, 8), (3, 4, 7)]
     for dim, k, L in cases:
@@ -533,6 +537,39 @@ def main():
             vt += e0.elapsed_time(e1) / 1e3
         vt /= vreps
         vcycle = {"value": N_total / vt, "unit": "DoF/s", "ms": vt * 1e3, "cuda_graph": True}
+    elif not shared:
+        # the decomposed V-cycle of the reference's unit cube at the same level
+        # (strong scaling of the secondary metric; one graph per rank)
+        nid = [pmg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        vctx = pmg.MultiGpuContext.for_rank(world, rank, local, nid[0], 3, args.degree, args.level, stack=1,
+                                            dtype=dt, variant=args.variant)
+        vctx.set_graph(True)
+        vx, vb = vctx.slab_tensor(0, "x"), vctx.slab_tensor(0, "b")
+        vx.copy_(torch.rand(vx.numel(), dtype=tdt, device="cuda", generator=gen) * 2 - 1)
+        vb.copy_(torch.rand(vb.numel(), dtype=tdt, device="cuda", generator=gen) * 2 - 1)
+        vstream = torch.cuda.ExternalStream(vctx.stream(0)[0])
+        vctx.v_cycle()
+        vctx.synchronize()
+        vreps = max(3, min(10, args.steps))
+        vt = 0.0
+        with torch.cuda.stream(vstream):
+            for _ in range(vreps):
+                barrier()
+                flush.fill_(1.0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(vstream)
+                vctx.v_cycle()
+                e1.record(vstream)
+                torch.cuda.synchronize()
+                vt += e0.elapsed_time(e1) / 1e3
+        t = torch.tensor([vt / vreps], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        vt = float(t.item())
+        nv = ((1 << args.level) * args.degree - 1) ** 3
+        vcycle = {"value": nv / vt, "unit": "DoF/s", "ms": vt * 1e3, "cuda_graph": True, "scaling": "strong",
+                  "workload": f"unit cube 2^{args.level} cells/dir over {world} z-slabs (pmg_dd_v_cycle)"}
+        del vctx
 
     # ---- e2e through the public API with host buffers (pinned) -----------------
     e2e_steps = max(3, min(args.steps, 20))
