@@ -19,6 +19,7 @@ from collections import defaultdict
 from bank_search import wavefronts
 
 PBS = {1: 16, 2: 8, 3: 4, 4: 2, 5: 2, 6: 1, 7: 1}
+WIDE = False
 
 
 def cost_of(instrs, word):
@@ -131,10 +132,13 @@ def best_layout(K, PB, X, fX, fY, word, budget):
                     best = (key, (tuple(s), size1))
     s, size1 = best[1]
     best2 = None
-    for pa in range(0, 9 if narr == 2 else 1):
+    # --wide: the pads over a full bank period (32 words), since the per-patch
+    # stride modulo the bank count decides where a warp's next patch lands
+    span = 33 if WIDE else 9
+    for pa in range(0, span if narr == 2 else 1):
         arrsep = size1 + pa
         tot1 = arrsep * (narr - 1) + size1
-        for pw in range(0, 9):
+        for pw in range(0, span):
             WW = tot1 + pw
             c = tensor_cost(K, PB, X, fX, fY, (s[0], s[1], s[2], WW), arrsep, word)
             key = (c, WW)
@@ -185,6 +189,9 @@ def ideal(K, PB, word):
 
 
 if __name__ == "__main__":
+    if "--wide" in sys.argv:
+        sys.argv.remove("--wide")
+        WIDE = True
     K = int(sys.argv[1])
     word = 8 if sys.argv[2] == "f64" else 4
     PB = int(sys.argv[3]) if len(sys.argv) > 3 else PBS[K]
