@@ -58,3 +58,33 @@ def test_onchip_roofline():
     assert B.onchip_roofline(2.0, 1.0, 1.0, B.B200) == pytest.approx(b200)
     with pytest.raises(ValueError):
         B.shared_traffic_model("global", 2, 3, 8)
+
+
+def test_pp_layout_tables_reproduce_their_modelled_wavefronts():
+    """The ping-pong smoother's shared-memory layouts (csrc/smoother_pp_table.hpp)
+    are what the bank model says they are: replaying every stage's warp
+    accesses (tools/bank_search_pp.py) gives the wavefront count recorded in
+    the table, within a bounded excess over the conflict-free ideal (the
+    measured counters are in profiles/r02/: LDS/STS 1.07-1.35x, LDGSTS
+    staging 2-3.8x)."""
+    import re
+    import sys
+
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import bank_search_pp as B
+
+    src = open(os.path.join(ROOT, "paper_2405_19004_b200", "csrc", "smoother_pp_table.hpp")).read()
+    blocks = re.findall(r"modelled (\d+) wavefronts per CTA, ideal (\d+) \(PB=(\d+)\).*?struct PPLayout<(\d), (\d)>"
+                        r".*?T\[6\]\[5\] = \{(.*?)\};.*?F\[7\] = \{(.*?)\};", src, re.S)
+    assert len(blocks) == 10
+    for modelled, ideal, PB, K, W, T, F in blocks:
+        K, W, PB = int(K), int(W), int(PB)
+        rows = [list(map(int, r.split(","))) for r in re.findall(r"\{([^{}]*)\}", T)]
+        flips = list(map(int, F.split(",")))
+        c = B.u_read_cost(K, PB, flips[0], W)
+        for i, X in enumerate("ABCDEF"):
+            s0, s1, s2, arrsep, WW = rows[i]
+            c += B.tensor_cost(K, PB, X, flips[i], flips[i + 1], (s0, s1, s2, WW), arrsep, W)
+        assert c == int(modelled), (K, W, c, modelled)
+        assert B.ideal(K, PB, W) == int(ideal)
+        assert c <= 1.3 * int(ideal), (K, W, c / int(ideal))
