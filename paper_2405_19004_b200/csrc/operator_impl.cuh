@@ -20,9 +20,14 @@
 // Band coefficients depend only on the lattice residue p mod k.
 #pragma once
 
-
-
 #include "common.cuh"
+
+// level_op3d_xb_kernel for k = 4 (profiles/r02/ab/level_op_xb.txt: residual
+// Q4 L7 f64 1.97 -> 1.89 ms, f32 1.48 -> 1.16 ms, Q4 L5 f64 0.056 -> 0.041 ms;
+// k = 3 is slower with it: 0.70 -> 1.21 ms, one CTA per SM at 157 registers)
+#ifndef PMG_OP_XB
+#define PMG_OP_XB 1
+#endif
 
 namespace pmgb
 {
@@ -336,6 +341,269 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
   }
 }
 
+// ---------------------------------------------------------------------------
+// 3D, k >= 3: one CELL per thread in x (xb = "x-blocked"). Lane l owns the K
+// consecutive output columns of one cell, starting at its vertex (lattice
+// residue 0), so every output's residue — and with it which band taps are
+// structurally zero — is a compile-time constant: dir 0 reads the 2K+1 window
+// [Kc - K, Kc + K] once for all K outputs (the vertex couples to the whole
+// window, the interior nodes of the cell only to its K+1 nodes) instead of
+// 2K+1 values per output. The tile row is stored with one pad word per K
+// columns, so the lanes' windows (stride K+1 words) are bank-conflict-free.
+// dir 1 (per-warp row residue, compile-time variant) and dir 2 (register
+// ring, compile-time plane residue) as in level_op3d_kernel.
+// ---------------------------------------------------------------------------
+template <int K, typename T>
+struct Op3XbCfg
+{
+  static constexpr int TX = 32, TY = 8, NT = TX * TY, W = 2 * K + 1;
+  static constexpr int XC = TX * K;                        // output columns of a tile
+  static constexpr int XW = XC + 2 * K, XH = TY + 2 * K;  // input tile
+  static constexpr int XWP = XW + XW / K + 1;              // padded row pitch (words)
+  static constexpr int ZCP = XC + XC / K + 1;              // padded dir-0 result row pitch
+  static constexpr int XN = XW * XH;
+  static constexpr int NLOAD = (XN + NT - 1) / NT;
+  static constexpr int ROWS = (XH + TY - 1) / TY;
+  static constexpr size_t SMEM = sizeof(T) * (3 * static_cast<size_t>(XH) * XWP + 4 * static_cast<size_t>(XH) * ZCP);
+};
+
+template <int K, typename T, int RES>
+__device__ __forceinline__ void opxb_dir1(const BandMats<T, K> &B, const T *zm, const T *za, int wy, int lane,
+                                          T (&wm)[K], T (&ws)[K])
+{
+  constexpr int W = 2 * K + 1, ZCP = Op3XbCfg<K, T>::ZCP;
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+  {
+    T a = T(0), b2 = T(0);
+#pragma unroll
+    for (int o = 0; o < W; ++o)
+    {
+      if (RES != 0 && (o < K - RES || o > 2 * K - RES))
+        continue;
+      const int pos = (wy + o) * ZCP + (K + 1) * lane + r;
+      const T vm = zm[pos], va = za[pos];
+      a = fma(B.M[RES][o], vm, a);
+      b2 = fma(B.A[RES][o], vm, fma(B.M[RES][o], va, b2));
+    }
+    wm[r] = a;
+    ws[r] = b2;
+  }
+}
+
+template <int K, typename T, int R = 0>
+__device__ __forceinline__ void opxb_dir1_res(const BandMats<T, K> &B, int res, const T *zm, const T *za, int wy,
+                                              int lane, T (&wm)[K], T (&ws)[K])
+{
+  if constexpr (R < K)
+  {
+    if (res == R)
+    {
+      opxb_dir1<K, T, R>(B, zm, za, wy, lane, wm, ws);
+      return;
+    }
+    opxb_dir1_res<K, T, R + 1>(B, res, zm, za, wy, lane, wm, ws);
+  }
+}
+
+template <int K, typename T, bool RESID>
+__global__ void __launch_bounds__(Op3XbCfg<K, T>::NT, 1)
+    level_op3d_xb_kernel(const __grid_constant__ BandMats<T, K> B, const T *__restrict__ x,
+                         const T *__restrict__ b, T *__restrict__ y, int64_t m, int zchunk, int64_t zbeg,
+                         int64_t zend)
+{
+  pdl_prologue();
+  using C = Op3XbCfg<K, T>;
+  constexpr int TX = C::TX, TY = C::TY, NT = C::NT, W = C::W, XW = C::XW, XH = C::XH, XN = C::XN;
+  constexpr int XWP = C::XWP, ZCP = C::ZCP, NLOAD = C::NLOAD, ROWS = C::ROWS;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T *Xs = reinterpret_cast<T *>(smraw);  // [3][XH][XWP]  input planes (padded rows)
+  T *ZM = Xs + 3 * XH * XWP;             // [2][XH][ZCP]
+  T *ZA = ZM + 2 * XH * ZCP;             // [2][XH][ZCP]
+
+  const int tid = threadIdx.x;
+  const int lane = tid % TX, wy = tid / TX;
+  // tile columns: X = x0 + K lane + r, x0 + 1 = K * 32 * bx (a vertex)
+  const int64_t x0 = static_cast<int64_t>(blockIdx.x) * C::XC - 1;
+  const int64_t g1 = static_cast<int64_t>(blockIdx.y) * TY;
+  const int64_t zs = (zbeg / K) * K + static_cast<int64_t>(blockIdx.z) * zchunk;
+  const int64_t ze = min(zs + zchunk, zend);
+  const int64_t m2 = m * m;
+  // tile slots: (row jr, column ir) -> padded smem position, global offset
+  int spos[NLOAD];
+  int64_t goff[NLOAD];
+  unsigned okm = 0;
+#pragma unroll
+  for (int j = 0; j < NLOAD; ++j)
+  {
+    const int e = tid + j * NT;
+    const int jr = e / XW, ir = e - (e / XW) * XW;
+    const int64_t gx = x0 - K + ir, gy = g1 - K + jr;
+    const bool ok = e < XN && gx >= 0 && gx < m && gy >= 0 && gy < m;
+    spos[j] = jr * XWP + ir + ir / K;
+    goff[j] = ok ? gy * m + gx : 0;
+    okm |= (ok ? 1u : 0u) << j;
+  }
+  const int64_t oy = g1 + wy;
+  const bool row_ok = oy < m;
+  const int res1 = static_cast<int>((oy + 1) % K);
+  const int NPL = static_cast<int>(ze - zs) + 2 * K;
+
+  auto issue = [&](int it) {
+    const int64_t q = zs - K + it;
+    const bool zin = q >= 0 && q < m && q >= zbeg - K;
+    T *dst = Xs + (it % 3) * XH * XWP;
+    const T *xq = x + (zin ? q : 0) * m2;
+#pragma unroll
+    for (int j = 0; j < NLOAD; ++j)
+    {
+      if (tid + j * NT < XN)
+        op_cp_async(dst + spos[j], xq + goff[j], zin && ((okm >> j) & 1u));
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  T acc[K][W];
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+#pragma unroll
+    for (int o = 0; o < W; ++o)
+      acc[r][o] = T(0);
+
+  issue(0);
+  if (NPL > 1)
+  {
+    issue(1);
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  }
+  else
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+
+  for (int base = 0; base < NPL; base += K)
+  {
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+    {
+      const int it = base + u;
+      if (it >= NPL)
+        break;
+      if (it + 2 < NPL)
+        issue(it + 2);
+      // b of this iteration's output plane into registers (used at the end)
+      const int64_t p_out = zs - 2 * K + it;
+      const bool out_it = it >= 2 * K && p_out < ze && p_out >= zbeg && row_ok;
+      T bv[K];
+      if constexpr (RESID)
+      {
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+        {
+          const int64_t X = x0 + K * lane + r;
+          bv[r] = (out_it && X >= 0 && X < m) ? __ldg(b + p_out * m2 + oy * m + X) : T(0);
+        }
+      }
+      // dir 0: the cell window of each row, K outputs with compile-time taps
+      const T *xs = Xs + (it % 3) * XH * XWP;
+      T *zm = ZM + (it & 1) * XH * ZCP;
+      T *za = ZA + (it & 1) * XH * ZCP;
+#pragma unroll
+      for (int rr = 0; rr < ROWS; ++rr)
+      {
+        const int j = wy + rr * TY;
+        if (j < XH)
+        {
+          const T *xr = xs + j * XWP + (K + 1) * lane;
+          T w[2 * K + 1];
+#pragma unroll
+          for (int q = 0; q <= 2 * K; ++q)
+            w[q] = xr[q + q / K];
+          T *zmr = zm + j * ZCP + (K + 1) * lane;
+          T *zar = za + j * ZCP + (K + 1) * lane;
+          {
+            T vm0 = B.M[0][0] * w[0], va0 = B.A[0][0] * w[0];
+            T vm1 = B.M[0][1] * w[1], va1 = B.A[0][1] * w[1];
+#pragma unroll
+            for (int q = 2; q <= 2 * K; q += 2)
+            {
+              vm0 = fma(B.M[0][q], w[q], vm0);
+              va0 = fma(B.A[0][q], w[q], va0);
+              if (q + 1 <= 2 * K)
+              {
+                vm1 = fma(B.M[0][q + 1], w[q + 1], vm1);
+                va1 = fma(B.A[0][q + 1], w[q + 1], va1);
+              }
+            }
+            zmr[0] = vm0 + vm1;
+            zar[0] = va0 + va1;
+          }
+#pragma unroll
+          for (int r = 1; r < K; ++r)
+          {
+            T vm = T(0), va = T(0);
+#pragma unroll
+            for (int q = K; q <= 2 * K; ++q)
+            {
+              vm = fma(B.M[r][q - r], w[q], vm);
+              va = fma(B.A[r][q - r], w[q], va);
+            }
+            zmr[r] = vm;
+            zar[r] = va;
+          }
+        }
+      }
+      if (it + 2 < NPL)
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
+      // dir 1 (the warp's row residue as a compile-time variant)
+      T wm[K], ws[K];
+      opxb_dir1_res<K, T>(B, res1, zm, za, wy, lane, wm, ws);
+      // dir 2: output plane p = q - K + jo, residue (u + 1 + jo) mod K,
+      // band offset 2K - jo; structurally zero taps dropped
+#pragma unroll
+      for (int jo = 0; jo < W; ++jo)
+      {
+        const int res = (u + 1 + jo) % K;
+        const int o = 2 * K - jo;
+        if (res != 0 && (o < K - res || o > 2 * K - res))
+          continue;
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+        {
+          acc[r][jo] = fma(B.A[res][o], wm[r], acc[r][jo]);
+          acc[r][jo] = fma(B.M[res][o], ws[r], acc[r][jo]);
+        }
+      }
+      if (out_it)
+      {
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+        {
+          const int64_t X = x0 + K * lane + r;
+          if (X >= 0 && X < m)
+          {
+            const int64_t idx = p_out * m2 + oy * m + X;
+            if constexpr (RESID)
+              y[idx] = bv[r] - acc[r][0];
+            else
+              y[idx] = acc[r][0];
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+      {
+#pragma unroll
+        for (int jo = 0; jo < W - 1; ++jo)
+          acc[r][jo] = acc[r][jo + 1];
+        acc[r][W - 1] = T(0);
+      }
+    }
+  }
+}
+
 // 2D: CTA = 128 columns marching down a chunk of rows that starts on a
 // multiple of K (so every row's lattice residue, and with it the dir-1 band
 // row, is a compile-time constant of the K-fold unrolled row loop: the
@@ -504,6 +772,31 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
     return;
   if constexpr (D == 3)
   {
+#if PMG_OP_XB
+    if constexpr (K == 4)
+    {
+      using CX = Op3XbCfg<K, T>;
+      const unsigned gxx = static_cast<unsigned>((m + 1 + CX::XC - 1) / CX::XC);
+      const unsigned gyx = static_cast<unsigned>((m + CX::TY - 1) / CX::TY);
+      const int64_t z0x = (zbeg / K) * K, spanx = zend - z0x;
+      int64_t nzx = (static_cast<int64_t>(sm_count) * 2 + gxx * gyx - 1) / (gxx * gyx);
+      int64_t zcx = std::max<int64_t>((spanx + nzx - 1) / nzx, 4 * K);
+      zcx = (zcx + K - 1) / K * K;
+      const unsigned gzx = static_cast<unsigned>((spanx + zcx - 1) / zcx);
+      auto kx = b ? level_op3d_xb_kernel<K, T, true> : level_op3d_xb_kernel<K, T, false>;
+      static unsigned xmask[2] = {0, 0};
+      if (first_on_device(xmask[b ? 1 : 0]))
+      {
+        check_cuda(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(CX::SMEM)),
+                   "cudaFuncSetAttribute(level_op3d_xb)");
+        check_cuda(cudaFuncSetAttribute(kx, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                   "cudaFuncSetAttribute(level_op3d_xb carveout)");
+      }
+      pdl_launch(kx, dim3(gxx, gyx, gzx), CX::NT, CX::SMEM, s, B, x, b, y, m, static_cast<int>(zcx), zbeg, zend);
+      check_launch("level_op3d_xb_kernel");
+      return;
+    }
+#endif
     using C = Op3Cfg<K, T>;
     constexpr size_t smem = C::SMEM;
     const unsigned gx = static_cast<unsigned>((m + C::TX - 1) / C::TX);
