@@ -146,9 +146,13 @@ def search(K, word, PB, NT):
     # coarse: search U and W parameters separately (their phases are disjoint
     # except p4_xold which only depends on U)
     bestU = None
-    for SU1 in range(NC, NC + 3):
-        for SU2 in range(NC * SU1, NC * SU1 + 5):
-            for UW in range(NC * SU2, NC * SU2 + 9):
+    # --wide: pads over a whole bank period (16 eight-byte / 32 four-byte banks)
+    wU = (16, 16, 24) if WIDE else (3, 5, 9)
+    for SU1 in range(NC, NC + wU[0]):
+        for SU2 in range(NC * SU1, NC * SU1 + wU[1]):
+            for UW in range(NC * SU2, NC * SU2 + wU[2]):
+                if WIDE and UW > UW_CAP:
+                    continue
                 L = Layout(K, PB, NT, UW, SU1, SU2, 2 * NC * NI2, NI2, NC * NI2)
                 _, _, per = cost(L, word, detail=True)
                 c = sum(per[k][0] for k in ("ldgsts", "p1_ld", "p4_xold"))
@@ -158,9 +162,12 @@ def search(K, word, PB, NT):
                     bestU = (key, (UW, SU1, SU2))
     UW, SU1, SU2 = bestU[1]
     bestW = None
-    for SJ in range(NI2, NI2 + 4):
-        for SW in range(NC * SJ, NC * SJ + 9):
-            for WW in range(SW + NC * SJ, SW + NC * SJ + 17):
+    wW = (17, 17, 33) if WIDE else (4, 9, 17)
+    for SJ in range(NI2, NI2 + wW[0]):
+        for SW in range(NC * SJ, NC * SJ + wW[1]):
+            for WW in range(SW + NC * SJ, SW + NC * SJ + wW[2]):
+                if WIDE and UW + WW > UW_CAP + WW_CAP:
+                    continue
                 L = Layout(K, PB, NT, UW, SU1, SU2, WW, SJ, SW)
                 _, _, per = cost(L, word, detail=True)
                 c = sum(per[k][0] for k in per if k.startswith(("p1_st", "p2", "p3", "p4_ld")))
@@ -172,7 +179,15 @@ def search(K, word, PB, NT):
     return L, cost(L, word, detail=True)
 
 
+WIDE = False
+# shared memory per patch (words) the wide search may use: 5 CTAs of PB = 16
+# patches per SM need UW + WW <= 354 (f64)
+UW_CAP, WW_CAP = 175, 175
+
 if __name__ == "__main__":
+    if "--wide" in sys.argv:
+        sys.argv.remove("--wide")
+        WIDE = True
     K = int(sys.argv[1])
     word = 8 if sys.argv[2] == "f64" else 4
     PB = int(sys.argv[3]) if len(sys.argv) > 3 else {1: 64, 2: 16, 3: 8}[K]
