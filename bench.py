@@ -578,13 +578,23 @@ def main():
         bh = torch.empty(N_total, dtype=tdt, pin_memory=True).numpy()
         xh[:] = x.cpu().numpy()
         bh[:] = b.cpu().numpy()
+        # the reference-facing C-ABI call itself (what the reference's smooth<T>
+        # forwards to): pmg_smooth_host(level, variant, x, b)
+        # = H2D of x, b, the colour kernels, D2H of x (pipelined)
+        import ctypes
+
+        from paper_2405_19004_b200._lib import VARIANTS
+
+        hx, hb, vcode = ctypes.c_void_p(xh.ctypes.data), ctypes.c_void_p(bh.ctypes.data), VARIANTS[args.variant]
         for _ in range(2):
-            pmg.smooth(lev, xh, bh, args.variant)
+            assert lib.pmg_smooth_host(lev.handle, vcode, hx, hb) == 0, lib.pmg_last_error()
         barrier()
+        st = 0
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            pmg.smooth(lev, xh, bh, args.variant)  # pmg_smooth_host: H2D x,b -> kernels -> D2H x
+            st |= lib.pmg_smooth_host(lev.handle, vcode, hx, hb)
         t_e2e = (time.perf_counter() - t0) / e2e_steps
+        assert st == 0, lib.pmg_last_error()
         h2d, d2h = 2 * N_total * word, N_total * word
     else:
         xh = torch.empty(x.numel(), dtype=tdt, pin_memory=True)
