@@ -161,6 +161,101 @@ void launch_f2d(const float *x, double *y, int64_t n, int sm_count, cudaStream_t
   check_launch("f2d_kernel");
 }
 
+// x = M b with M stored column-major (Mt[j][i] = M[i][j], the V-cycle's
+// response to the unit vector e_j): CTA = 32 rows x 8 column groups, fixed
+// reduction order (deterministic)
+template <typename T>
+__global__ void __launch_bounds__(256) coarse_gemv_kernel(const T *__restrict__ Mt, const T *__restrict__ b,
+                                                         T *__restrict__ x, int n)
+{
+  pdl_prologue();
+  __shared__ T part[8][32];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  T acc = T(0);
+  if (i < n)
+    for (int j = grp; j < n; j += 8)
+      acc = fma(Mt[static_cast<int64_t>(j) * n + i], b[j], acc);
+  part[grp][lane] = acc;
+  __syncthreads();
+  if (grp == 0 && i < n)
+  {
+    T s = part[0][lane];
+#pragma unroll
+    for (int g = 1; g < 8; ++g)
+      s += part[g][lane];
+    x[i] = s;
+  }
+}
+
+template <typename T>
+__global__ void unit_kernel(T *x, int n, int j)
+{
+  pdl_prologue();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = i == j ? T(1) : T(0);
+}
+
+// e_j with j read from device memory (column counter of a replayed graph)
+template <typename T>
+__global__ void unit_dev_kernel(T *x, int n, const int *__restrict__ j)
+{
+  pdl_prologue();
+  const int jj = *j;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = i == jj ? T(1) : T(0);
+}
+
+// column *j of Mt = v, then ++*j (one CTA: the increment follows every read)
+template <typename T>
+__global__ void __launch_bounds__(1024) store_column_kernel(T *__restrict__ Mt, const T *__restrict__ v, int n, int *j)
+{
+  pdl_prologue();
+  const int jj = *j;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    Mt[static_cast<int64_t>(jj) * n + i] = v[i];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    *j = jj + 1;
+}
+
+template <typename T>
+void launch_unit_dev(T *x, int n, const int *j, cudaStream_t s)
+{
+  pdl_launch(unit_dev_kernel<T>, dim3((n + 255) / 256), dim3(256), 0, s, x, n, j);
+  check_launch("unit_dev_kernel");
+}
+
+template <typename T>
+void launch_store_column(T *Mt, const T *v, int n, int *j, cudaStream_t s)
+{
+  pdl_launch(store_column_kernel<T>, dim3(1), dim3(1024), 0, s, Mt, v, n, j);
+  check_launch("store_column_kernel");
+}
+
+template void launch_unit_dev<double>(double *, int, const int *, cudaStream_t);
+template void launch_unit_dev<float>(float *, int, const int *, cudaStream_t);
+template void launch_store_column<double>(double *, const double *, int, int *, cudaStream_t);
+template void launch_store_column<float>(float *, const float *, int, int *, cudaStream_t);
+
+template <typename T>
+void launch_coarse_gemv(const T *Mt, const T *b, T *x, int n, cudaStream_t s)
+{
+  pdl_launch(coarse_gemv_kernel<T>, dim3((n + 31) / 32), dim3(256), 0, s, Mt, b, x, n);
+  check_launch("coarse_gemv_kernel");
+}
+
+template <typename T>
+void launch_unit(T *x, int n, int j, cudaStream_t s)
+{
+  pdl_launch(unit_kernel<T>, dim3((n + 255) / 256), dim3(256), 0, s, x, n, j);
+  check_launch("unit_kernel");
+}
+
+template void launch_coarse_gemv<double>(const double *, const double *, double *, int, cudaStream_t);
+template void launch_coarse_gemv<float>(const float *, const float *, float *, int, cudaStream_t);
+template void launch_unit<double>(double *, int, int, cudaStream_t);
+template void launch_unit<float>(float *, int, int, cudaStream_t);
 template void launch_dot<double>(const double *, const double *, int64_t, double *, double *, bool, cudaStream_t);
 template void launch_dot<float>(const float *, const float *, int64_t, double *, double *, bool, cudaStream_t);
 template void launch_fill<double>(double *, int64_t, double, int, cudaStream_t);

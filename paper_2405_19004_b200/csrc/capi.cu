@@ -138,6 +138,14 @@ struct pmg_mg_s
   std::vector<DevBuf *> r_ws, bc_ws, xc_ws;  // per level li (sizes: N_li, N_{li-1}, N_{li-1})
   CachedGraph graph;
   cudaStream_t cap_stream = nullptr;
+  // coarse V-cycle operator: the V-cycle of level index mat_li (<= MAT_MAX_N
+  // unknowns) from a zero initial guess is a fixed linear map b -> x; its
+  // matrix (columns = responses to e_j, computed by running that V-cycle) is
+  // applied as one GEMV where the recursion reaches mat_li
+  int mat_li = -1;
+  bool mat_ready = false;
+  unsigned mat_key = 0;
+  DevBuf mat, mat_b, mat_x;
   DevBuf fmg_x[32];
   GmresWork gmres;
   ~pmg_mg_s()
@@ -522,6 +530,88 @@ void apply_smoother(pmg_mg_s *mg, pmg_level_s *lev, T *x, const T *b, cudaStream
 }
 
 template <typename T>
+void vcycle_impl(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s);
+
+// what the coarse matrix depends on: smoother organisation, variant, sweeps
+unsigned coarse_mat_key(const pmg_mg_s *mg)
+{
+  return static_cast<unsigned>(smoother_impl_choice()) | (static_cast<unsigned>(mg->variant & 0xff) << 4) |
+         (static_cast<unsigned>(mg->pre & 0xff) << 12) | (static_cast<unsigned>(mg->post & 0xff) << 20);
+}
+
+// the V-cycle of level index li with a ZERO initial guess (the recursion's
+// coarse correction, multigrid.cpp:335-338): one GEMV with the precomputed
+// operator on the coarse-matrix level, the recursive cycle otherwise
+template <typename T>
+void coarse_correction(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s)
+{
+  if (li == mg->mat_li && mg->mat_ready && mg->mat_key == coarse_mat_key(mg))
+  {
+    launch_coarse_gemv<T>(mg->mat.as<T>(), b, x, static_cast<int>(mg->levels[li]->S.N), s);
+    return;
+  }
+  vcycle_impl<T>(mg, li, x, b, s);
+}
+
+// (re)build the coarse operator eagerly (never inside a stream capture): N
+// V-cycles on the unit vectors, column j = V(e_j)
+template <typename T>
+void ensure_coarse_matrix(pmg_mg_s *mg, cudaStream_t s, bool for_finest = false)
+{
+  if (mg->mat_li < 0)
+    return;
+  // on the finest level only a coarse correction from outside uses it
+  if (mg->mat_li == static_cast<int>(mg->levels.size()) - 1 && !for_finest)
+    return;
+  const unsigned key = coarse_mat_key(mg);
+  if (mg->mat_ready && mg->mat_key == key)
+    return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  check_cuda(cudaStreamIsCapturing(s, &cs), "capture status");
+  if (cs != cudaStreamCaptureStatusNone)
+    return;  // not ready: the recursion is used (consistent within this call)
+  const int n = static_cast<int>(mg->levels[mg->mat_li]->S.N);
+  mg->mat_ready = false;
+  mg->mat.ensure(static_cast<size_t>(n) * n * sizeof(T));
+  mg->mat_b.ensure(static_cast<size_t>(n) * sizeof(T));
+  mg->mat_x.ensure(static_cast<size_t>(n) * sizeof(T) + 16);
+  T *M = mg->mat.as<T>(), *eb = mg->mat_b.as<T>(), *ex = mg->mat_x.as<T>();
+  int *col = reinterpret_cast<int *>(ex + n);  // column counter after x (16 B slack)
+  // one column step (e_j, V-cycle from 0, store, ++j) captured once and
+  // replayed n times
+  check_cuda(cudaMemsetAsync(col, 0, sizeof(int), s), "column counter");
+  check_cuda(cudaStreamSynchronize(s), "coarse matrix");
+  if (!mg->cap_stream)
+    check_cuda(cudaStreamCreateWithFlags(&mg->cap_stream, cudaStreamNonBlocking), "stream");
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  check_cuda(cudaStreamBeginCapture(mg->cap_stream, cudaStreamCaptureModeRelaxed), "capture begin");
+  try
+  {
+    launch_unit_dev<T>(eb, n, col, mg->cap_stream);
+    launch_fill<T>(ex, n, T(0), mg->levels[mg->mat_li]->sm_count, mg->cap_stream);
+    vcycle_impl<T>(mg, mg->mat_li, ex, eb, mg->cap_stream);
+    launch_store_column<T>(M, ex, n, col, mg->cap_stream);
+  }
+  catch (...)
+  {
+    cudaStreamEndCapture(mg->cap_stream, &graph);
+    if (graph)
+      cudaGraphDestroy(graph);
+    throw;
+  }
+  check_cuda(cudaStreamEndCapture(mg->cap_stream, &graph), "capture end");
+  check_cuda(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+  cudaGraphDestroy(graph);
+  for (int j = 0; j < n; ++j)
+    check_cuda(cudaGraphLaunch(exec, mg->cap_stream), "graph launch");
+  check_cuda(cudaStreamSynchronize(mg->cap_stream), "coarse matrix");
+  cudaGraphExecDestroy(exec);
+  mg->mat_key = key;
+  mg->mat_ready = true;
+}
+
+template <typename T>
 void vcycle_impl(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s)
 {
   pmg_level_s *lev = mg->levels[li];
@@ -541,7 +631,7 @@ void vcycle_impl(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s)
   ktab<T>(lev).level_op(lev->band_mats.data(), x, b, r, lev->S.m, lev->sm_count, s);
   // b_c = R r and x_c = 0 in the same launch (the coarse solve zeroes x itself)
   restrict_impl<T>(crs, lev, r, bc, s, li - 1 > 0 ? xc : nullptr);
-  vcycle_impl<T>(mg, li - 1, xc, bc, s);
+  coarse_correction<T>(mg, li - 1, xc, bc, s);
   prolongate_impl<T>(crs, lev, xc, x, true, s);
   for (int i = 0; i < mg->post; ++i)
     apply_smoother<T>(mg, lev, x, b, s);
@@ -550,6 +640,7 @@ void vcycle_impl(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s)
 template <typename T>
 void vcycle_entry(pmg_mg_s *mg, int li, T *x, const T *b, bool use_graph, cudaStream_t s)
 {
+  ensure_coarse_matrix<T>(mg, s);
   if (!use_graph)
   {
     vcycle_impl<T>(mg, li, x, b, s);
@@ -774,12 +865,35 @@ void mg_residual_finest(pmg_mg h, const double *x, const double *b, double *r, c
 
 void mg_vcycle_f32(pmg_mg h, int li, float *x, const float *b, cudaStream_t s)
 {
+  ensure_coarse_matrix<float>(h, s);
   vcycle_impl<float>(h, li, x, b, s);
 }
 
 void mg_vcycle_f64(pmg_mg h, int li, double *x, const double *b, cudaStream_t s)
 {
+  ensure_coarse_matrix<double>(h, s);
   vcycle_impl<double>(h, li, x, b, s);
+}
+
+void mg_coarse_correction(pmg_mg h, int li, void *x, const void *b, bool use_graph, cudaStream_t s)
+{
+  DevScope dg(h->device);
+  if (h->dtype == PMG_F64)
+  {
+    ensure_coarse_matrix<double>(h, s, true);
+    if (li == h->mat_li && h->mat_ready)
+      coarse_correction<double>(h, li, static_cast<double *>(x), static_cast<const double *>(b), s);
+    else
+      vcycle_entry<double>(h, li, static_cast<double *>(x), static_cast<const double *>(b), use_graph, s);
+  }
+  else
+  {
+    ensure_coarse_matrix<float>(h, s, true);
+    if (li == h->mat_li && h->mat_ready)
+      coarse_correction<float>(h, li, static_cast<float *>(x), static_cast<const float *>(b), s);
+    else
+      vcycle_entry<float>(h, li, static_cast<float *>(x), static_cast<const float *>(b), use_graph, s);
+  }
 }
 
 }  // namespace pmgb
@@ -1393,6 +1507,22 @@ int pmg_mg_create_kind(int dim, int degree, int finest_level, int dtype, int var
           transfer_scratch<float>(mg->levels[li]);
       }
     }
+    // coarse-matrix level: the largest li >= 1 with <= PMG_COARSE_MAT_N
+    // unknowns (the parent's coarse correction becomes one GEMV; 1331
+    // measured best: 3375-unknown operators, 91 MB, are slower to stream than
+    // the recursion they replace, profiles/r02/ab/coarse_matrix.txt)
+    {
+      static const int64_t nmax = [] {
+        const char *e = std::getenv("PMG_COARSE_MAT_N");
+        return e ? std::atoll(e) : int64_t(1331);
+      }();
+      // (the finest level too: the slab decomposition's agglomerated coarse
+      // correction may land there; the same level is then chosen in every
+      // context that holds it, so all of them compute it the same way)
+      for (int li = 1; li < static_cast<int>(mg->levels.size()); ++li)
+        if (mg->levels[li]->S.N <= nmax)
+          mg->mat_li = li;
+    }
     // the reference assembles a CSR matrix per level (multigrid.cpp:37-41):
     // same nonzero budget (std::runtime_error), front lists built up front
     if (kind == PMG_POINT_GS)
@@ -1467,8 +1597,10 @@ int pmg_v_cycle_host(pmg_mg h, int li, void *x, const void *b)
     void *dx = io.dev(0, bytes), *db = io.dev(1, bytes);
     io.h2d(dx, x, bytes);
     io.h2d(db, b, bytes);
-    PMG_DISPATCH_T(h, vcycle_impl<T>(h, li, static_cast<T *>(dx), static_cast<const T *>(db),
-                                     l->io_stream));
+    PMG_DISPATCH_T(h, {
+      ensure_coarse_matrix<T>(h, l->io_stream);
+      vcycle_impl<T>(h, li, static_cast<T *>(dx), static_cast<const T *>(db), l->io_stream);
+    });
     io.d2h(x, dx, bytes);
     io.sync();
   });
@@ -1498,6 +1630,7 @@ int pmg_full_multigrid(pmg_mg h, const void *const *rhs, void *x, double tol, in
       xl[li] = h->fmg_x[li].as<T>();
     }
     xl[L] = static_cast<T *>(x);
+    ensure_coarse_matrix<T>(h, s);
     vcycle_impl<T>(h, 0, xl[0], static_cast<const T *>(rhs[0]), s);
     for (int li = 1; li <= L; ++li)
     {

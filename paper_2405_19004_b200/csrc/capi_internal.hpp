@@ -115,5 +115,10 @@ void mg_apply_finest_op(pmg_mg h, const double *x, double *y, cudaStream_t s);
 void mg_residual_finest(pmg_mg h, const double *x, const double *b, double *r, cudaStream_t s);
 void mg_vcycle_f32(pmg_mg h, int li, float *x, const float *b, cudaStream_t s);
 void mg_vcycle_f64(pmg_mg h, int li, double *x, const double *b, cudaStream_t s);
+// the V-cycle of level index li from x = 0 (the recursion's coarse
+// correction): the precomputed coarse operator where it applies, else the
+// (graph-)V-cycle; used by the slab decomposition's agglomerated levels so they
+// compute what the single-device recursion computes
+void mg_coarse_correction(pmg_mg h, int li, void *x, const void *b, bool use_graph, cudaStream_t s);
 
 }  // namespace pmgb

@@ -720,9 +720,9 @@ void vcycle_level(pmg_dd_s *d, int lev)
       DevScope g(root->device);
       // the recursion starts from x_c = 0 (multigrid.cpp:336)
       check_cuda(cudaMemsetAsync(root->L[lev].a[A_XC], 0, d->bytes(d->mz(cl) * d->ps(cl)), root->main), "x_c = 0");
-      ck(pmg_v_cycle(root->root_mg, cl - 1, root->L[lev].a[A_XC], root->L[lev].a[A_BC], d->capturing ? 0 : 1,
-                     root->main),
-         "dd coarse V-cycle");
+      // as the single-device recursion does it (multigrid.cpp:335-338)
+      mg_coarse_correction(root->root_mg, cl - 1, root->L[lev].a[A_XC], root->L[lev].a[A_BC], !d->capturing,
+                           root->main);
     }
     broadcast_from_root(d, lev, A_XC, d->mz(cl) * d->ps(cl));
   }
