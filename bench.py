@@ -485,7 +485,7 @@ def main():
     max_mhz = peaks.get("sm_max_mhz", 1965.0)
     fp_peak = sm_count * (64 if args.dtype == "f64" else 128) * 2 * max_mhz * 1e6 / 1e12
     traffic, traffic_note = None, None
-    if os.path.exists(NCU_SUMMARY):
+    if world == 1 and os.path.exists(NCU_SUMMARY):  # the capture is of the single-GPU step
         try:
             s = json.load(open(NCU_SUMMARY))
             key = f"d{args.dim}k{args.degree}L{args.level}{args.dtype}{args.variant}"
