@@ -75,6 +75,32 @@ __device__ __forceinline__ bool pp_line(int tid, int &p, int &a, int &b)
   return true;
 }
 
+// the same map with the lane order given explicitly
+template <int K, typename T, int NA, int NB, bool FLIP>
+__device__ __forceinline__ bool pp_line_f(int tid, int &p, int &a, int &b)
+{
+  constexpr int PB = PPCfg<K, T>::PB;
+  if (tid >= PB * NA * NB)
+    return false;
+  p = tid / (NA * NB);
+  const int rr = tid - p * (NA * NB);
+  if constexpr (FLIP)
+  {
+    a = rr / NB;
+    b = rr - a * NB;
+  }
+  else
+  {
+    b = rr / NA;
+    a = rr - b * NA;
+  }
+  return true;
+}
+
+#ifndef PMG_PP_MAPS
+#define PMG_PP_MAPS 1
+#endif
+
 template <int K, typename T, int MODE>
 __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
     vp_smooth_pp_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ ColorArgs<T> a)
@@ -194,8 +220,35 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
   __syncthreads();
 
   int p, la, lb;
+#if PMG_PP_MAPS
+  // the stages' thread -> (patch, line) maps, computed once (the compiler does
+  // not carry them across the barriers: ~9% of the f32 k = 3 instructions were
+  // these divisions, recomputed per stage); stages C..G share one map per lane
+  // order
+  struct LineMap
+  {
+    int p, a, b;
+    bool on;
+  };
+  LineMap mA, mB, mC0, mC1;
+  mA.on = pp_line<K, T, A_, NC, NC>(tid, mA.p, mA.a, mA.b);
+  mB.on = pp_line<K, T, B_, NI, NC>(tid, mB.p, mB.a, mB.b);
+  mC0.on = pp_line_f<K, T, NI, NI, false>(tid, mC0.p, mC0.a, mC0.b);
+  mC1.on = pp_line_f<K, T, NI, NI, true>(tid, mC1.p, mC1.a, mC1.b);
+  using PL = PPLayout<K, sizeof(T)>;
+  auto use = [&](const LineMap &mm) {
+    p = mm.p;
+    la = mm.a;
+    lb = mm.b;
+    return mm.on;
+  };
+#define PP_LINE(S, NA, NB)                                                                                 \
+  ((S) == A_ ? use(mA) : (S) == B_ ? use(mB) : (PL::f(S) ? use(mC1) : use(mC0)))
+#else
+#define PP_LINE(S, NA, NB) pp_line<K, T, S, NA, NB>(tid, p, la, lb)
+#endif
   // ---- A: U along t0 -> zM = M0 u, zA = A0 u  (lines (j1, j2)) -----------------
-  if (pp_line<K, T, A_, NC, NC>(tid, p, la, lb))
+  if (PP_LINE(A_, NC, NC))
   {
     const T *u_ = U + p * UW + NC * la + NC * NC * lb;
     T u[NC], ue[K + 1], uo[K], zm[NI], za[NI];
@@ -214,7 +267,7 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
   }
   __syncthreads();
   // ---- B: along j1: wMM = M1 zM, wS = A1 zM + M1 zA  (lines (i0, j2)) ------------
-  if (pp_line<K, T, B_, NI, NC>(tid, p, la, lb))
+  if (PP_LINE(B_, NI, NC))
   {
     T zm[NC], za[NC];
 #pragma unroll
@@ -237,7 +290,7 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
   }
   __syncthreads();
   // ---- C: along j2: r = b - (A2 wMM + M2 wS); S^T r  (lines (i0, i1)) -----------
-  if (pp_line<K, T, C_, NI, NI>(tid, p, la, lb))
+  if (PP_LINE(C_, NI, NI))
   {
     T wm[NC], ws[NC];
 #pragma unroll
@@ -261,7 +314,7 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
   }
   __syncthreads();
   // ---- D: along i1: S^T  (lines (i0, c2)) -----------------------------------------
-  if (pp_line<K, T, D_, NI, NI>(tid, p, la, lb))
+  if (PP_LINE(D_, NI, NI))
   {
     T v[NI], y[NI];
 #pragma unroll
@@ -274,7 +327,7 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
   }
   __syncthreads();
   // ---- E: along i0: S^T, x 1/(lambda sums), S  (lines (c1, c2)) -------------------
-  if (pp_line<K, T, E_, NI, NI>(tid, p, la, lb))
+  if (PP_LINE(E_, NI, NI))
   {
     T v[NI], y[NI];
 #pragma unroll
@@ -292,7 +345,7 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
   }
   __syncthreads();
   // ---- F: along c1: S  (lines (i0, c2)) -------------------------------------------
-  if (pp_line<K, T, F_, NI, NI>(tid, p, la, lb))
+  if (PP_LINE(F_, NI, NI))
   {
     T v[NI], y[NI];
 #pragma unroll
@@ -305,7 +358,7 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
   }
   __syncthreads();
   // ---- G: along c2: S, x^I update  (lines (i0, i1)) -------------------------------
-  if (pp_line<K, T, G_, NI, NI>(tid, p, la, lb) && bt * PB + p < a.total)
+  if (PP_LINE(G_, NI, NI) && bt * PB + p < a.total)
   {
     T v[NI], y[NI];
 #pragma unroll
@@ -325,6 +378,8 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
     }
   }
 }
+
+#undef PP_LINE
 
 template <int K, typename T, int MODE>
 void launch_vp_smooth_pp(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a, cudaStream_t s)
