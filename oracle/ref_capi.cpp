@@ -282,6 +282,31 @@ void ref_mg_set_threads(void *p, int threads)
     h->f->threads = threads;
 }
 
+// MultigridContext::pre_smooth / post_smooth / variant (multigrid.hpp:37-40)
+void ref_mg_set_smoothing(void *p, int pre, int post)
+{
+  auto *h = static_cast<RefMg *>(p);
+  if (h->d)
+  {
+    h->d->pre_smooth = pre;
+    h->d->post_smooth = post;
+  }
+  if (h->f)
+  {
+    h->f->pre_smooth = pre;
+    h->f->post_smooth = post;
+  }
+}
+
+void ref_mg_set_variant(void *p, int variant)
+{
+  auto *h = static_cast<RefMg *>(p);
+  if (h->d)
+    h->d->variant = static_cast<SmootherVariant>(variant);
+  if (h->f)
+    h->f->variant = static_cast<SmootherVariant>(variant);
+}
+
 int64_t ref_mg_total_dofs(void *p, int li)
 {
   auto *h = static_cast<RefMg *>(p);

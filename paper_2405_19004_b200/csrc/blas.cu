@@ -6,6 +6,8 @@
 // reproducible run to run (no atomics), accumulated in f64.
 #include "blas.cuh"
 
+#include <type_traits>
+
 namespace pmgb
 {
 
@@ -161,31 +163,59 @@ void launch_f2d(const float *x, double *y, int64_t n, int sm_count, cudaStream_t
   check_launch("f2d_kernel");
 }
 
-// x = M b with M stored column-major (Mt[j][i] = M[i][j], the V-cycle's
-// response to the unit vector e_j): CTA = 32 rows x 8 column groups, fixed
-// reduction order (deterministic)
+// x = M b with the coarse V-cycle operator M (n x n, row-major, row pitch
+// ld = n rounded up to 4, zero padded): one warp per row streams the row in
+// 16-byte vectors (4 independent accumulators in flight per lane), b through
+// the read-only path, then a fixed shuffle tree (deterministic). The operator
+// is streamed once per application, so this is an HBM (or L2) copy-rate kernel.
 template <typename T>
-__global__ void __launch_bounds__(256) coarse_gemv_kernel(const T *__restrict__ Mt, const T *__restrict__ b,
-                                                         T *__restrict__ x, int n)
+__global__ void __launch_bounds__(256) coarse_gemv_kernel(const T *__restrict__ M, const T *__restrict__ b,
+                                                         T *__restrict__ x, int n, int ld)
 {
   pdl_prologue();
-  __shared__ T part[8][32];
-  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  const int i = blockIdx.x * 32 + lane;
-  T acc = T(0);
-  if (i < n)
-    for (int j = grp; j < n; j += 8)
-      acc = fma(Mt[static_cast<int64_t>(j) * n + i], b[j], acc);
-  part[grp][lane] = acc;
-  __syncthreads();
-  if (grp == 0 && i < n)
+  using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+  constexpr int W = 16 / sizeof(T);
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= n)
+    return;
+  const V *mr = reinterpret_cast<const V *>(M + static_cast<int64_t>(row) * ld);
+  const int nv = n / W;  // full vectors inside the row (b is read unpadded)
+  T acc[4] = {T(0), T(0), T(0), T(0)};
+  int c = lane;
+  for (; c + 96 < nv; c += 128)
   {
-    T s = part[0][lane];
+    V mv[4];
 #pragma unroll
-    for (int g = 1; g < 8; ++g)
-      s += part[g][lane];
-    x[i] = s;
+    for (int u = 0; u < 4; ++u)
+      mv[u] = __ldg(mr + c + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+    {
+      const T *mm = reinterpret_cast<const T *>(&mv[u]);
+      const T *bb = b + (c + 32 * u) * W;
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        acc[u] = fma(mm[w], __ldg(bb + w), acc[u]);
+    }
   }
+  for (; c < nv; c += 32)
+  {
+    const V mv = __ldg(mr + c);
+    const T *mm = reinterpret_cast<const T *>(&mv);
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      acc[0] = fma(mm[w], __ldg(b + c * W + w), acc[0]);
+  }
+  const int j = nv * W + lane;  // scalar tail
+  if (j < n)
+    acc[1] = fma(M[static_cast<int64_t>(row) * ld + j], __ldg(b + j), acc[1]);
+  T sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0)
+    x[row] = sum;
 }
 
 template <typename T>
@@ -206,14 +236,16 @@ __global__ void unit_dev_kernel(T *x, int n, const int *__restrict__ j)
     x[i] = i == jj ? T(1) : T(0);
 }
 
-// column *j of Mt = v, then ++*j (one CTA: the increment follows every read)
+// column *j of M (row pitch ld) = v, then ++*j (one CTA: the increment
+// follows every read)
 template <typename T>
-__global__ void __launch_bounds__(1024) store_column_kernel(T *__restrict__ Mt, const T *__restrict__ v, int n, int *j)
+__global__ void __launch_bounds__(1024) store_column_kernel(T *__restrict__ M, const T *__restrict__ v, int n, int ld,
+                                                            int *j)
 {
   pdl_prologue();
   const int jj = *j;
   for (int i = threadIdx.x; i < n; i += blockDim.x)
-    Mt[static_cast<int64_t>(jj) * n + i] = v[i];
+    M[static_cast<int64_t>(i) * ld + jj] = v[i];
   __syncthreads();
   if (threadIdx.x == 0)
     *j = jj + 1;
@@ -227,21 +259,21 @@ void launch_unit_dev(T *x, int n, const int *j, cudaStream_t s)
 }
 
 template <typename T>
-void launch_store_column(T *Mt, const T *v, int n, int *j, cudaStream_t s)
+void launch_store_column(T *M, const T *v, int n, int ld, int *j, cudaStream_t s)
 {
-  pdl_launch(store_column_kernel<T>, dim3(1), dim3(1024), 0, s, Mt, v, n, j);
+  pdl_launch(store_column_kernel<T>, dim3(1), dim3(1024), 0, s, M, v, n, ld, j);
   check_launch("store_column_kernel");
 }
 
 template void launch_unit_dev<double>(double *, int, const int *, cudaStream_t);
 template void launch_unit_dev<float>(float *, int, const int *, cudaStream_t);
-template void launch_store_column<double>(double *, const double *, int, int *, cudaStream_t);
-template void launch_store_column<float>(float *, const float *, int, int *, cudaStream_t);
+template void launch_store_column<double>(double *, const double *, int, int, int *, cudaStream_t);
+template void launch_store_column<float>(float *, const float *, int, int, int *, cudaStream_t);
 
 template <typename T>
-void launch_coarse_gemv(const T *Mt, const T *b, T *x, int n, cudaStream_t s)
+void launch_coarse_gemv(const T *M, const T *b, T *x, int n, int ld, cudaStream_t s)
 {
-  pdl_launch(coarse_gemv_kernel<T>, dim3((n + 31) / 32), dim3(256), 0, s, Mt, b, x, n);
+  pdl_launch(coarse_gemv_kernel<T>, dim3((n + 7) / 8), dim3(256), 0, s, M, b, x, n, ld);
   check_launch("coarse_gemv_kernel");
 }
 
@@ -252,8 +284,8 @@ void launch_unit(T *x, int n, int j, cudaStream_t s)
   check_launch("unit_kernel");
 }
 
-template void launch_coarse_gemv<double>(const double *, const double *, double *, int, cudaStream_t);
-template void launch_coarse_gemv<float>(const float *, const float *, float *, int, cudaStream_t);
+template void launch_coarse_gemv<double>(const double *, const double *, double *, int, int, cudaStream_t);
+template void launch_coarse_gemv<float>(const float *, const float *, float *, int, int, cudaStream_t);
 template void launch_unit<double>(double *, int, int, cudaStream_t);
 template void launch_unit<float>(float *, int, int, cudaStream_t);
 template void launch_dot<double>(const double *, const double *, int64_t, double *, double *, bool, cudaStream_t);

@@ -539,6 +539,9 @@ unsigned coarse_mat_key(const pmg_mg_s *mg)
          (static_cast<unsigned>(mg->pre & 0xff) << 12) | (static_cast<unsigned>(mg->post & 0xff) << 20);
 }
 
+// row pitch of the coarse operator (16-byte rows for the GEMV's vector loads)
+inline int coarse_mat_ld(int n) { return (n + 3) & ~3; }
+
 // the V-cycle of level index li with a ZERO initial guess (the recursion's
 // coarse correction, multigrid.cpp:335-338): one GEMV with the precomputed
 // operator on the coarse-matrix level, the recursive cycle otherwise
@@ -547,7 +550,8 @@ void coarse_correction(pmg_mg_s *mg, int li, T *x, const T *b, cudaStream_t s)
 {
   if (li == mg->mat_li && mg->mat_ready && mg->mat_key == coarse_mat_key(mg))
   {
-    launch_coarse_gemv<T>(mg->mat.as<T>(), b, x, static_cast<int>(mg->levels[li]->S.N), s);
+    const int n = static_cast<int>(mg->levels[li]->S.N);
+    launch_coarse_gemv<T>(mg->mat.as<T>(), b, x, n, coarse_mat_ld(n), s);
     return;
   }
   vcycle_impl<T>(mg, li, x, b, s);
@@ -572,7 +576,8 @@ void ensure_coarse_matrix(pmg_mg_s *mg, cudaStream_t s, bool for_finest = false)
     return;  // not ready: the recursion is used (consistent within this call)
   const int n = static_cast<int>(mg->levels[mg->mat_li]->S.N);
   mg->mat_ready = false;
-  mg->mat.ensure(static_cast<size_t>(n) * n * sizeof(T));
+  const int ld = coarse_mat_ld(n);
+  mg->mat.ensure(static_cast<size_t>(n) * ld * sizeof(T));
   mg->mat_b.ensure(static_cast<size_t>(n) * sizeof(T));
   mg->mat_x.ensure(static_cast<size_t>(n) * sizeof(T) + 16);
   T *M = mg->mat.as<T>(), *eb = mg->mat_b.as<T>(), *ex = mg->mat_x.as<T>();
@@ -580,6 +585,7 @@ void ensure_coarse_matrix(pmg_mg_s *mg, cudaStream_t s, bool for_finest = false)
   // one column step (e_j, V-cycle from 0, store, ++j) captured once and
   // replayed n times
   check_cuda(cudaMemsetAsync(col, 0, sizeof(int), s), "column counter");
+  check_cuda(cudaMemsetAsync(M, 0, static_cast<size_t>(n) * ld * sizeof(T), s), "coarse matrix pad");
   check_cuda(cudaStreamSynchronize(s), "coarse matrix");
   if (!mg->cap_stream)
     check_cuda(cudaStreamCreateWithFlags(&mg->cap_stream, cudaStreamNonBlocking), "stream");
@@ -591,7 +597,7 @@ void ensure_coarse_matrix(pmg_mg_s *mg, cudaStream_t s, bool for_finest = false)
     launch_unit_dev<T>(eb, n, col, mg->cap_stream);
     launch_fill<T>(ex, n, T(0), mg->levels[mg->mat_li]->sm_count, mg->cap_stream);
     vcycle_impl<T>(mg, mg->mat_li, ex, eb, mg->cap_stream);
-    launch_store_column<T>(M, ex, n, col, mg->cap_stream);
+    launch_store_column<T>(M, ex, n, ld, col, mg->cap_stream);
   }
   catch (...)
   {
@@ -1508,13 +1514,14 @@ int pmg_mg_create_kind(int dim, int degree, int finest_level, int dtype, int var
       }
     }
     // coarse-matrix level: the largest li >= 1 with <= PMG_COARSE_MAT_N
-    // unknowns (the parent's coarse correction becomes one GEMV; 1331
-    // measured best: 3375-unknown operators, 91 MB, are slower to stream than
-    // the recursion they replace, profiles/r02/ab/coarse_matrix.txt)
+    // unknowns (the parent's coarse correction becomes one GEMV). 3375
+    // unknowns (91 MB f64) stream in ~15 us with the warp-per-row GEMV, less
+    // than the recursion they replace; the next levels (k = 2: 29791
+    // unknowns, 7 GB) are far beyond (profiles/r02/ab/coarse_matrix*.txt)
     {
       static const int64_t nmax = [] {
         const char *e = std::getenv("PMG_COARSE_MAT_N");
-        return e ? std::atoll(e) : int64_t(1331);
+        return e ? std::atoll(e) : int64_t(3375);
       }();
       // (the finest level too: the slab decomposition's agglomerated coarse
       // correction may land there; the same level is then chosen in every

@@ -36,6 +36,8 @@ def lib():
             "ref_point_gs": (i, [vp, i, vp, vp]),
             "ref_assemble_sparse": (i, [i, i, i, vp, vp, vp, ctypes.POINTER(ctypes.c_int64)]),
             "ref_mg_set_threads": (None, [vp, i]),
+            "ref_mg_set_smoothing": (None, [vp, i, i]),
+            "ref_mg_set_variant": (None, [vp, i]),
             "ref_mg_total_dofs": (i64, [vp, i]),
             "ref_smooth": (i, [vp, i, i, vp, vp]),
             "ref_apply_laplacian": (i, [vp, i, vp, vp]),
@@ -92,6 +94,12 @@ class RefMg:
 
     def set_threads(self, t):
         lib().ref_mg_set_threads(self.h, t)
+
+    def set_smoothing(self, pre, post):
+        lib().ref_mg_set_smoothing(self.h, pre, post)
+
+    def set_variant(self, variant):
+        lib().ref_mg_set_variant(self.h, VARIANT[variant])
 
     def n(self, li):
         return lib().ref_mg_total_dofs(self.h, li)
