@@ -20,6 +20,8 @@
 // Band coefficients depend only on the lattice residue p mod k.
 #pragma once
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 // level_op3d_xb_kernel for k = 4 (profiles/r02/ab/level_op_xb.txt: residual
@@ -51,14 +53,34 @@ struct Op3Cfg
 #ifndef PMG_OP_TY
 #define PMG_OP_TY 8
 #endif
+#ifndef PMG_OP_NB
+#define PMG_OP_NB 3
+#endif
   static constexpr int TX = 32, TY = PMG_OP_TY, NT = TX * TY, W = 2 * K + 1;
+  static constexpr int NB = PMG_OP_NB;  // input-plane ring (NB - 1 planes in flight)
   static constexpr int XW = TX + 2 * K, XH = TY + 2 * K, XN = XW * XH;
   static constexpr int NLOAD = (XN + NT - 1) / NT;   // tile slots per thread
   static constexpr int ROWS = (XH + TY - 1) / TY;    // dir-0 rows per thread
   static constexpr bool C1REG = K <= 2;              // dir-1 band row in registers
   static constexpr size_t SMEM =
-      sizeof(T) * (3 * static_cast<size_t>(XN) + 3 * NT + 4 * static_cast<size_t>(XH) * TX + 2 * K * W);
+      sizeof(T) * (NB * static_cast<size_t>(XN) + NB * NT + 4 * static_cast<size_t>(XH) * TX + 2 * K * W);
 };
+
+// cp.async.wait_group with a run-time count (0..7)
+__device__ __forceinline__ void cp_wait_groups(int n)
+{
+  switch (n)
+  {
+  case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+  case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+  case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+  case 3: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
+  case 4: asm volatile("cp.async.wait_group 4;\n" ::: "memory"); break;
+  case 5: asm volatile("cp.async.wait_group 5;\n" ::: "memory"); break;
+  case 6: asm volatile("cp.async.wait_group 6;\n" ::: "memory"); break;
+  default: asm volatile("cp.async.wait_group 7;\n" ::: "memory"); break;
+  }
+}
 
 template <int K, typename T>
 constexpr size_t op3d_smem()
@@ -80,10 +102,13 @@ __device__ __forceinline__ void op_cp_async(T *smem, const T *gmem, bool valid)
 
 // two resident CTAs per SM for k >= 3 (measured: register-capped 128 beats
 // the unconstrained 130-214 registers; for k <= 2 the compiler's choice wins)
+#ifndef PMG_OP_MINB_LO
+#define PMG_OP_MINB_LO 1
+#endif
 template <int K>
 constexpr int op3d_minb()
 {
-  return K >= 3 ? 2 : 1;
+  return K >= 3 ? 2 : PMG_OP_MINB_LO;
 }
 
 // dir 1 for a warp whose rows have lattice residue RES: rows of residue
@@ -138,11 +163,11 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
   pdl_prologue();
   using C = Op3Cfg<K, T>;
   constexpr int TX = C::TX, TY = C::TY, NT = C::NT, W = C::W, XW = C::XW, XH = C::XH, XN = C::XN;
-  constexpr int NLOAD = C::NLOAD, ROWS = C::ROWS;
+  constexpr int NLOAD = C::NLOAD, ROWS = C::ROWS, NB = C::NB;
   extern __shared__ __align__(16) unsigned char smraw[];
-  T *Xs = reinterpret_cast<T *>(smraw);  // [3][XH][XW]  input planes
-  T *Bv = Xs + 3 * XN;                   // [3][NT]      b of the output planes
-  T *ZM = Bv + 3 * NT;                   // [2][XH][TX]
+  T *Xs = reinterpret_cast<T *>(smraw);  // [NB][XH][XW]  input planes
+  T *Bv = Xs + NB * XN;                  // [NB][NT]      b of the output planes
+  T *ZM = Bv + NB * NT;                  // [2][XH][TX]
   T *ZA = ZM + 2 * XH * TX;              // [2][XH][TX]
   T *bm = ZA + 2 * XH * TX;              // [K][W]
   T *ba = bm + K * W;
@@ -206,7 +231,7 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
     // planes below zbeg - K feed only outputs below zbeg (never stored): not
     // read, so a slab caller need only hold planes from zbeg - K
     const bool zin = q >= 0 && q < m && q >= zbeg - K;
-    T *dst = Xs + (it % 3) * XN;
+    T *dst = Xs + (it % NB) * XN;
     const T *xq = x + (zin ? q : 0) * m2;
 #pragma unroll
     for (int j = 0; j < NLOAD; ++j)
@@ -222,7 +247,7 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
     {
       const int64_t p = q - K;
       const bool ok = out_ok && it >= 2 * K && p < ze && p >= zbeg;
-      op_cp_async(Bv + (it % 3) * NT + tid, ok ? b + p * m2 + out_off : b, ok);
+      op_cp_async(Bv + (it % NB) * NT + tid, ok ? b + p * m2 + out_off : b, ok);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -232,14 +257,11 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
   for (int o = 0; o < W; ++o)
     acc[o] = T(0);
 
-  issue(0);
-  if (NPL > 1)
-  {
-    issue(1);
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-  }
-  else
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  // planes 0 .. NB-2 in flight; wait for plane 0
+  const int npre = min(NB - 1, NPL);
+  for (int it = 0; it < npre; ++it)
+    issue(it);
+  cp_wait_groups(npre - 1);
   __syncthreads();
 
   for (int base = 0; base < NPL; base += K)
@@ -250,10 +272,10 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
       const int it = base + u;  // uniform across the CTA
       if (it >= NPL)
         break;
-      if (it + 2 < NPL)
-        issue(it + 2);
+      if (it + NB - 1 < NPL)
+        issue(it + NB - 1);
       // dir 0
-      const T *xs = Xs + (it % 3) * XN;
+      const T *xs = Xs + (it % NB) * XN;
       T *zm = ZM + (it & 1) * XH * TX;
       T *za = ZA + (it & 1) * XH * TX;
 #pragma unroll
@@ -281,10 +303,8 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
           za[j * TX + lane] = va0 + va1;
         }
       }
-      if (it + 2 < NPL)
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      else
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      // plane it + 1 complete (groups issued after it may stay in flight)
+      cp_wait_groups(max(0, min(it + NB - 1, NPL - 1) - (it + 1)));
       __syncthreads();
       // dir 1
       T wm = T(0), ws = T(0);
@@ -329,7 +349,7 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
       {
         const int64_t idx = p_out * m2 + out_off;
         if constexpr (RESID)
-          y[idx] = Bv[(it % 3) * NT + tid] - acc[0];
+          y[idx] = Bv[(it % NB) * NT + tid] - acc[0];
         else
           y[idx] = acc[0];
       }
@@ -337,6 +357,251 @@ __global__ void __launch_bounds__(Op3Cfg<K, T>::NT, op3d_minb<K>())
       for (int jo = 0; jo < W - 1; ++jo)
         acc[jo] = acc[jo + 1];
       acc[W - 1] = T(0);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3D, k <= 2: register-blocked ("cb" = cell-blocked). Lane l of warp w owns
+// the K columns of one cell (nodes X0 + K l .. X0 + K l + K - 1, lattice
+// residues 0 .. K-1) on BY consecutive rows (residues i mod K): per input
+// plane it streams the BY + 2K rows of its 3K-wide window from the staged
+// tile through registers — dir 0 (compile-time residue, structurally zero
+// taps dropped) straight into the dir-1 sums of the rows it feeds — so the
+// dir-0 results never round-trip through shared memory and dir 1 reads
+// nothing. dir 2 is the register ring of level_op3d_kernel. The per-output
+// shared traffic drops from ~30 words to (BY + 2K) 3K / (BY K) (9 words at
+// k = 2): level_op3d_kernel is bound by shared-memory wavefronts at k <= 2
+// (f64 C2 L6 residual 35.8 us = 21% of HBM, the same at 2-4 CTAs per SM).
+// The tile row is stored with one pad word per K columns (K = 2: lane stride
+// 3 words), conflict-free. One barrier per plane.
+// ---------------------------------------------------------------------------
+#ifndef PMG_OP_CB
+#define PMG_OP_CB 1
+#endif
+#ifndef PMG_OP_CB_NW
+#define PMG_OP_CB_NW 4
+#endif
+template <int K, typename T>
+struct Op3CbCfg
+{
+  static constexpr int NW = PMG_OP_CB_NW, NT = 32 * NW, W = 2 * K + 1;
+  static constexpr int BY = K == 1 ? 4 : 2;          // rows per thread (a multiple of K)
+  static constexpr int XC = 32 * K, YC = NW * BY;    // output nodes of a tile
+  static constexpr int XW = XC + 2 * K, XH = YC + 2 * K;
+  static constexpr int XWP = K == 1 ? XW : XW + XW / K + 1;  // padded pitch
+  static constexpr int XN = XW * XH, NLOAD = (XN + NT - 1) / NT;
+  static constexpr int OUT = BY * K;  // outputs per thread per plane
+  static constexpr size_t SMEM = sizeof(T) * (3 * static_cast<size_t>(XH) * XWP + 3 * static_cast<size_t>(OUT) * NT);
+  static_assert(BY % K == 0, "rows per thread: whole cells");
+};
+
+// shared column of tile column X
+template <int K>
+__device__ __forceinline__ constexpr int cb_pos(int X)
+{
+  return K == 1 ? X : X + X / K;
+}
+
+template <int K, typename T, bool RESID>
+__global__ void __launch_bounds__(Op3CbCfg<K, T>::NT)
+    level_op3d_cb_kernel(const __grid_constant__ BandMats<T, K> B, const T *__restrict__ x,
+                         const T *__restrict__ b, T *__restrict__ y, int64_t m, int zchunk, int64_t zbeg,
+                         int64_t zend)
+{
+  pdl_prologue();
+  using C = Op3CbCfg<K, T>;
+  constexpr int NT = C::NT, W = C::W, BY = C::BY, XW = C::XW, XH = C::XH, XWP = C::XWP, XN = C::XN;
+  constexpr int NLOAD = C::NLOAD, OUT = C::OUT;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T *Xs = reinterpret_cast<T *>(smraw);  // [3][XH][XWP]  input planes
+  T *Bv = Xs + 3 * XH * XWP;             // [3][OUT][NT]  b of the thread's outputs
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wy = tid >> 5;
+  // tile origin in node coordinates (node = interior index + 1)
+  const int X0 = static_cast<int>(blockIdx.x) * C::XC;
+  const int Y0 = static_cast<int>(blockIdx.y) * C::YC;
+  const int64_t zs = (zbeg / K) * K + static_cast<int64_t>(blockIdx.z) * zchunk;  // multiple of K
+  const int64_t ze = min(zs + zchunk, zend);
+  const int64_t m2 = m * m;
+  const int mi = static_cast<int>(m);
+
+  int off[NLOAD], dpos[NLOAD];
+  unsigned okm = 0;
+#pragma unroll
+  for (int j = 0; j < NLOAD; ++j)
+  {
+    const int e = tid + j * NT;
+    const int jr = e / XW, X = e - jr * XW;
+    const int ix = X0 - K + X - 1, iy = Y0 - K + jr - 1;  // interior indices
+    const bool ok = e < XN && ix >= 0 && ix < mi && iy >= 0 && iy < mi;
+    off[j] = ok ? iy * mi + ix : 0;
+    dpos[j] = jr * XWP + cb_pos<K>(X);
+    okm |= (ok ? 1u : 0u) << j;
+  }
+  // this thread's outputs (i, r): interior (iy0 + i, ix0 + r)
+  const int ix0 = X0 + K * lane - 1, iy0 = Y0 + BY * wy - 1;
+  unsigned outm = 0;
+#pragma unroll
+  for (int i = 0; i < BY; ++i)
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+    {
+      const bool ok = ix0 + r >= 0 && ix0 + r < mi && iy0 + i >= 0 && iy0 + i < mi;
+      outm |= (ok ? 1u : 0u) << (i * K + r);
+    }
+  const int NPL = static_cast<int>(ze - zs) + 2 * K;  // input planes zs-K .. ze+K-1
+
+  auto issue = [&](int it) {
+    const int64_t q = zs - K + it;
+    const bool zin = q >= 0 && q < m && q >= zbeg - K;
+    T *dst = Xs + (it % 3) * XH * XWP;
+    const T *xq = x + (zin ? q : 0) * m2;
+#pragma unroll
+    for (int j = 0; j < NLOAD; ++j)
+    {
+      const int e = tid + j * NT;
+      if (e < XN)
+        op_cp_async(dst + dpos[j], xq + off[j], zin && ((okm >> j) & 1u));
+    }
+    if constexpr (RESID)
+    {
+      const int64_t p = q - K;
+      const bool okp = it >= 2 * K && p < ze && p >= zbeg;
+#pragma unroll
+      for (int i = 0; i < BY; ++i)
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+        {
+          const bool ok = okp && ((outm >> (i * K + r)) & 1u);
+          op_cp_async(Bv + ((it % 3) * OUT + i * K + r) * NT + tid,
+                      ok ? b + p * m2 + static_cast<int64_t>(iy0 + i) * m + (ix0 + r) : b, ok);
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  T acc[W][BY][K];
+#pragma unroll
+  for (int o = 0; o < W; ++o)
+#pragma unroll
+    for (int i = 0; i < BY; ++i)
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        acc[o][i][r] = T(0);
+
+  issue(0);
+  if (NPL > 1)
+  {
+    issue(1);
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+  }
+  else
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+
+  for (int base = 0; base < NPL; base += K)
+  {
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+    {
+      const int it = base + u;  // uniform across the CTA
+      if (it >= NPL)
+        break;
+      if (it + 2 < NPL)
+        issue(it + 2);
+      const T *xs = Xs + (it % 3) * XH * XWP + (wy * BY) * XWP + cb_pos<K>(K * lane);
+      // dir 0 row by row, each row straight into the dir-1 sums it feeds
+      T wm[BY][K], ws[BY][K];
+#pragma unroll
+      for (int i = 0; i < BY; ++i)
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+        {
+          wm[i][r] = T(0);
+          ws[i][r] = T(0);
+        }
+#pragma unroll
+      for (int jr = 0; jr < BY + 2 * K; ++jr)
+      {
+        T v[3 * K];
+#pragma unroll
+        for (int t = 0; t < 3 * K; ++t)
+          v[t] = xs[jr * XWP + (K == 1 ? t : t + t / K)];
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+        {
+          // output column residue r: input window v[r + o], o in [0, 2K]
+          T zm = T(0), za = T(0);
+#pragma unroll
+          for (int o = 0; o < W; ++o)
+          {
+            if (r != 0 && (o < K - r || o > 2 * K - r))
+              continue;
+            zm = fma(B.M[r][o], v[r + o], zm);
+            za = fma(B.A[r][o], v[r + o], za);
+          }
+#pragma unroll
+          for (int i = 0; i < BY; ++i)
+          {
+            const int o = jr - i;  // band offset of input row jr for output row i
+            const int ry = i % K;
+            if (o < 0 || o > 2 * K || (ry != 0 && (o < K - ry || o > 2 * K - ry)))
+              continue;
+            wm[i][r] = fma(B.M[ry][o], zm, wm[i][r]);
+            ws[i][r] = fma(B.A[ry][o], zm, fma(B.M[ry][o], za, ws[i][r]));
+          }
+        }
+      }
+      // dir 2: output plane p = q - K + jo, residue (u + 1 + jo) mod K, band
+      // offset 2K - jo
+#pragma unroll
+      for (int jo = 0; jo < W; ++jo)
+      {
+        const int res = (u + 1 + jo) % K;
+        const int o = 2 * K - jo;
+        if (res != 0 && (o < K - res || o > 2 * K - res))
+          continue;
+#pragma unroll
+        for (int i = 0; i < BY; ++i)
+#pragma unroll
+          for (int r = 0; r < K; ++r)
+            acc[jo][i][r] = fma(B.A[res][o], wm[i][r], fma(B.M[res][o], ws[i][r], acc[jo][i][r]));
+      }
+      const int64_t p_out = zs - 2 * K + it;
+      if (it >= 2 * K && p_out < ze && p_out >= zbeg)
+      {
+#pragma unroll
+        for (int i = 0; i < BY; ++i)
+#pragma unroll
+          for (int r = 0; r < K; ++r)
+            if ((outm >> (i * K + r)) & 1u)
+            {
+              const int64_t idx = p_out * m2 + static_cast<int64_t>(iy0 + i) * m + (ix0 + r);
+              if constexpr (RESID)
+                y[idx] = Bv[((it % 3) * OUT + i * K + r) * NT + tid] - acc[0][i][r];
+              else
+                y[idx] = acc[0][i][r];
+            }
+      }
+#pragma unroll
+      for (int jo = 0; jo < W - 1; ++jo)
+#pragma unroll
+        for (int i = 0; i < BY; ++i)
+#pragma unroll
+          for (int r = 0; r < K; ++r)
+            acc[jo][i][r] = acc[jo + 1][i][r];
+#pragma unroll
+      for (int i = 0; i < BY; ++i)
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+          acc[W - 1][i][r] = T(0);
+      if (it + 2 < NPL)
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
     }
   }
 }
@@ -797,6 +1062,39 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
       return;
     }
 #endif
+#if PMG_OP_CB
+    if constexpr (K <= 2)
+    {
+      using CB = Op3CbCfg<K, T>;
+      static const int cb_ctas = [] {
+        const char *e = std::getenv("PMG_OP_CB_CTAS");
+        return e ? std::max(1, std::atoi(e)) : 4;
+      }();
+      static const int cb_zmin = [] {
+        const char *e = std::getenv("PMG_OP_CB_ZMIN");
+        return e ? std::max(1, std::atoi(e)) : 2;
+      }();
+      const unsigned gxc = static_cast<unsigned>((m + 1 + CB::XC - 1) / CB::XC);
+      const unsigned gyc = static_cast<unsigned>((m + 1 + CB::YC - 1) / CB::YC);
+      const int64_t z0c = (zbeg / K) * K, spanc = zend - z0c;
+      const int64_t nzc = (static_cast<int64_t>(sm_count) * cb_ctas + gxc * gyc - 1) / (gxc * gyc);
+      int64_t zcc = std::max<int64_t>((spanc + nzc - 1) / nzc, cb_zmin * K);
+      zcc = (zcc + K - 1) / K * K;
+      const unsigned gzc = static_cast<unsigned>((spanc + zcc - 1) / zcc);
+      auto kc = b ? level_op3d_cb_kernel<K, T, true> : level_op3d_cb_kernel<K, T, false>;
+      static unsigned cmask[2] = {0, 0};
+      if (first_on_device(cmask[b ? 1 : 0]))
+      {
+        check_cuda(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(CB::SMEM)),
+                   "cudaFuncSetAttribute(level_op3d_cb)");
+        check_cuda(cudaFuncSetAttribute(kc, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                   "cudaFuncSetAttribute(level_op3d_cb carveout)");
+      }
+      pdl_launch(kc, dim3(gxc, gyc, gzc), CB::NT, CB::SMEM, s, B, x, b, y, m, static_cast<int>(zcc), zbeg, zend);
+      check_launch("level_op3d_cb_kernel");
+      return;
+    }
+#endif
     using C = Op3Cfg<K, T>;
     constexpr size_t smem = C::SMEM;
     const unsigned gx = static_cast<unsigned>((m + C::TX - 1) / C::TX);
@@ -804,10 +1102,18 @@ void launch_level_op(const BandMats<T, K> &B, const T *x, const T *b, T *y, int6
     // z chunk (a multiple of K): enough CTAs for ~6 per SM, >= 4k planes to
     // bound the recomputed halo
     const int64_t z0 = (zbeg / K) * K, span = zend - z0;
-    int64_t want = static_cast<int64_t>(sm_count) * 6;
+    static const int zmin_k = [] {
+      const char *e = std::getenv("PMG_OP_ZMIN");
+      return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    static const int ctas = [] {
+      const char *e = std::getenv("PMG_OP_CTAS");
+      return e ? std::max(1, std::atoi(e)) : 6;
+    }();
+    int64_t want = static_cast<int64_t>(sm_count) * ctas;
     int64_t nz = (want + gx * gy - 1) / (gx * gy);
     int64_t zchunk = (span + nz - 1) / nz;
-    zchunk = std::max<int64_t>(zchunk, 4 * K);
+    zchunk = std::max<int64_t>(zchunk, zmin_k * K);
     zchunk = (zchunk + K - 1) / K * K;
     const unsigned gz = static_cast<unsigned>((span + zchunk - 1) / zchunk);
     auto kern = b ? level_op3d_kernel<K, T, true> : level_op3d_kernel<K, T, false>;

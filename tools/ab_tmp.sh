@@ -1,5 +1,7 @@
-O=gpurun_out/ab_cm; mkdir -p $O
-for r in 1 2; do for n in 1331 3375; do echo "== $n" >> $O/qt.log
-PMG_COARSE_MAT_N=$n timeout 300 python tools/quick_time.py 3 2 6 f64 fused 3 2 6 f32 fused 3 1 6 f64 fused 3 4 5 f64 fused 3 2 7 f64 fused 3 4 6 f32 fused >> $O/qt.log 2>&1; done; done
-for n in 1331 3375; do PMG_COARSE_MAT_N=$n timeout 600 python bench.py --steps 20 --warmup 5 --no-sweep --no-cpu > $O/bench_$n.json 2> $O/bench_$n.err; done
-PMG_COARSE_MAT_N=3375 timeout 900 python -m pytest tests/ -x -q -m gpu -k "vcycle or v_cycle or coarse or fmg or dd or gmres" > $O/tests.log 2>&1; tail -3 $O/tests.log
+O=gpurun_out/ab_cb2; mkdir -p $O
+run() { timeout 600 ncu --nvtx --nvtx-include "vc/" --metrics gpu__time_duration.sum,launch__grid_size --clock-control none --cache-control none --csv --log-file $O/$1.csv python tools/debug/vc_kernels.py $2 > $O/$1.log 2>&1; }
+for lib in b200 mb6 fly flymb6 nw8; do for c in 4 8; do
+PMG_OP_CB_CTAS=$c PMG_B200_LIB=$PWD/paper_2405_19004_b200/libpmg_$lib.so run ${lib}_c${c}_c2 "3 2 6 f64"
+PMG_OP_CB_CTAS=$c PMG_B200_LIB=$PWD/paper_2405_19004_b200/libpmg_$lib.so run ${lib}_c${c}_k2L7 "3 2 7 f64"
+PMG_OP_CB_CTAS=$c PMG_B200_LIB=$PWD/paper_2405_19004_b200/libpmg_$lib.so run ${lib}_c${c}_f32 "3 2 6 f32"
+done; done
