@@ -164,52 +164,78 @@ void launch_f2d(const float *x, double *y, int64_t n, int sm_count, cudaStream_t
 }
 
 // x = M b with the coarse V-cycle operator M (n x n, row-major, row pitch
-// ld = n rounded up to 4, zero padded): one warp per row streams the row in
-// 16-byte vectors (4 independent accumulators in flight per lane), b through
-// the read-only path, then a fixed shuffle tree (deterministic). The operator
-// is streamed once per application, so this is an HBM (or L2) copy-rate kernel.
+// ld = n rounded up to 4, zero padded). One warp per row streams the row in
+// 16-byte vectors, two batches of 4 per lane in flight (software-pipelined),
+// evict-first (the operator is read once per application and should not
+// displace the level vectors in L2); b is staged once per CTA in shared
+// memory; fixed shuffle-tree reduction (deterministic). The first batch is
+// issued before the programmatic-dependency wait: M is not written by the
+// predecessor kernel, so its stream starts while that kernel drains.
 template <typename T>
 __global__ void __launch_bounds__(256) coarse_gemv_kernel(const T *__restrict__ M, const T *__restrict__ b,
                                                          T *__restrict__ x, int n, int ld)
 {
-  pdl_prologue();
   using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
-  constexpr int W = 16 / sizeof(T);
+  constexpr int W = 16 / sizeof(T), U = 4;
+  extern __shared__ __align__(16) unsigned char gemv_smem[];
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= n)
-    return;
-  const V *mr = reinterpret_cast<const V *>(M + static_cast<int64_t>(row) * ld);
-  const int nv = n / W;  // full vectors inside the row (b is read unpadded)
-  T acc[4] = {T(0), T(0), T(0), T(0)};
-  int c = lane;
-  for (; c + 96 < nv; c += 128)
+  const bool active = row < n;
+  const V *mr = reinterpret_cast<const V *>(M + static_cast<int64_t>(active ? row : 0) * ld);
+  const int nv = ld / W;
+  const int nfull = nv / (32 * U);  // full U-batches of this row
+  V cur[U], nxt[U];
+  if (active && nfull > 0)
   {
-    V mv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      mv[u] = __ldg(mr + c + 32 * u);
+    for (int u = 0; u < U; ++u)
+      cur[u] = __ldcs(mr + lane + 32 * u);
+  }
+  pdl_prologue();
+  T *bs = reinterpret_cast<T *>(gemv_smem);  // [ld], zero padded
+  for (int j = threadIdx.x; j < ld; j += blockDim.x)
+    bs[j] = j < n ? b[j] : T(0);
+  __syncthreads();
+  if (!active)
+    return;
+  const V *bv = reinterpret_cast<const V *>(bs);
+  T acc[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < U; ++u)
+    acc[u] = T(0);
+  for (int t = 0; t < nfull; ++t)
+  {
+    const int c = lane + 32 * U * t;
+    if (t + 1 < nfull)
     {
-      const T *mm = reinterpret_cast<const T *>(&mv[u]);
-      const T *bb = b + (c + 32 * u) * W;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        nxt[u] = __ldcs(mr + c + 32 * U + 32 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+    {
+      const V bb = bv[c + 32 * u];
+      const T *mm = reinterpret_cast<const T *>(&cur[u]);
+      const T *bq = reinterpret_cast<const T *>(&bb);
 #pragma unroll
       for (int w = 0; w < W; ++w)
-        acc[u] = fma(mm[w], __ldg(bb + w), acc[u]);
+        acc[u] = fma(mm[w], bq[w], acc[u]);
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      cur[u] = nxt[u];
   }
-  for (; c < nv; c += 32)
+  for (int c = lane + 32 * U * nfull; c < nv; c += 32)
   {
-    const V mv = __ldg(mr + c);
+    const V mv = __ldcs(mr + c);
+    const V bb = bv[c];
     const T *mm = reinterpret_cast<const T *>(&mv);
+    const T *bq = reinterpret_cast<const T *>(&bb);
 #pragma unroll
     for (int w = 0; w < W; ++w)
-      acc[0] = fma(mm[w], __ldg(b + c * W + w), acc[0]);
+      acc[0] = fma(mm[w], bq[w], acc[0]);
   }
-  const int j = nv * W + lane;  // scalar tail
-  if (j < n)
-    acc[1] = fma(M[static_cast<int64_t>(row) * ld + j], __ldg(b + j), acc[1]);
   T sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
@@ -273,7 +299,12 @@ template void launch_store_column<float>(float *, const float *, int, int, int *
 template <typename T>
 void launch_coarse_gemv(const T *M, const T *b, T *x, int n, int ld, cudaStream_t s)
 {
-  pdl_launch(coarse_gemv_kernel<T>, dim3((n + 7) / 8), dim3(256), 0, s, M, b, x, n, ld);
+  const size_t smem = static_cast<size_t>(ld) * sizeof(T);
+  static unsigned attr_mask = 0;
+  if (first_on_device(attr_mask))
+    check_cuda(cudaFuncSetAttribute(coarse_gemv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024),
+               "cudaFuncSetAttribute(coarse_gemv)");
+  pdl_launch(coarse_gemv_kernel<T>, dim3((n + 7) / 8), dim3(256), smem, s, M, b, x, n, ld);
   check_launch("coarse_gemv_kernel");
 }
 

@@ -1521,7 +1521,8 @@ int pmg_mg_create_kind(int dim, int degree, int finest_level, int dtype, int var
     {
       static const int64_t nmax = [] {
         const char *e = std::getenv("PMG_COARSE_MAT_N");
-        return e ? std::atoll(e) : int64_t(3375);
+        // (<= 12000: the GEMV stages b in <= 96 KB of shared memory)
+        return e ? std::min<int64_t>(std::atoll(e), 12000) : int64_t(3375);
       }();
       // (the finest level too: the slab decomposition's agglomerated coarse
       // correction may land there; the same level is then chosen in every
