@@ -354,7 +354,9 @@ __global__ void __launch_bounds__(Rest3Cfg<K>::NT)
   using C = Rest3Cfg<K>;
   constexpr int CX = C::CX, CY = C::CY, OX = C::OX, OY = C::OY, WX = C::WX, WY = C::WY, NT = C::NT;
   __shared__ T Ps[2 * K + 1][K + 1];
-  __shared__ __align__(16) T F[2][WY * WX];
+  // fine-plane ring: NB - 1 planes in flight (static shared memory <= 48 KB)
+  constexpr int NB = (3 * WY * WX + WY * OX) * sizeof(T) <= 46 * 1024 ? 3 : 2;
+  __shared__ __align__(16) T F[NB][WY * WX];
   __shared__ T R1[WY][OX];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   for (int e = tid; e < (2 * K + 1) * (K + 1); e += NT)
@@ -397,6 +399,8 @@ __global__ void __launch_bounds__(Rest3Cfg<K>::NT)
   T acc[K + 1], carry = T(0);
   const int nplanes = (c_hi - c_lo + 1) * 2 * K;
   stage(0, 2 * c_lo * K);
+  if (NB == 3 && nplanes > 1)
+    stage(1, 2 * c_lo * K + 1);
   int s = 0;
   for (int cz = c_lo; cz <= c_hi; ++cz)
   {
@@ -406,11 +410,17 @@ __global__ void __launch_bounds__(Rest3Cfg<K>::NT)
 #pragma unroll
     for (int r = 1; r <= 2 * K; ++r, ++s)
     {
-      const int buf = s & 1;
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      const int buf = s % NB;
+      // plane s landed (with NB = 3, plane s + 1 may stay in flight)
+      if (NB == 3 && s + 1 < nplanes)
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       __syncthreads();
-      if (s + 1 < nplanes)
-        stage(buf ^ 1, 2 * cz * K + r);  // next plane: 0-based index of lattice 2czK + r + 1
+      // plane s + NB - 1 (0-based fine plane 2 c_lo K + s + NB - 1) into the
+      // buffer of plane s - 1, whose x pass ended before the previous barrier
+      if (s + NB - 1 < nplanes)
+        stage((s + NB - 1) % NB, 2 * c_lo * K + s + NB - 1);
       // x pass: R1[fy][ox] for the tile's coarse x nodes
       if (tx < OX)
       {
@@ -653,10 +663,18 @@ void launch_prolongate(const ProlMats<T, K> &P, const T *xc, T *xf, bool acc, in
 // passes). Below that the per-plane staging latency of the march (2k planes
 // per cell in sequence) exceeds three fully parallel passes; for k = 3, 5-7
 // the y-window halo (CY = 2 or 1 cells) costs more than the saved traffic.
+inline int64_t restrict3d_min_nodes()
+{
+  static const int64_t v = [] {
+    const char *e = std::getenv("PMG_RESTRICT3D_MIN");
+    return e ? static_cast<int64_t>(std::atoll(e)) : int64_t(96);
+  }();
+  return v;
+}
 template <int K>
 inline bool use_restrict3d(int64_t mc)
 {
-  return use_fused_transfer() && (K == 1 || K == 2 || K == 4) && 2 * mc + 1 >= 96;
+  return use_fused_transfer() && (K == 1 || K == 2 || K == 4) && 2 * mc + 1 >= restrict3d_min_nodes();
 }
 
 // coarse z-nodes [q0, q1) (0-based) of R r_f in one launch; chunks of the

@@ -14,6 +14,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import paper_2405_19004_b200 as pmg  # noqa: E402
 
 dim, k, L, dtype = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+if os.environ.get("PMG_IMPL"):
+    pmg.set_smoother_impl(os.environ["PMG_IMPL"])
 dt = np.float64 if dtype == "f64" else np.float32
 tdt = torch.float64 if dtype == "f64" else torch.float32
 ctx = pmg.make_multigrid_context(dim, k, L, "fused", dtype=dt)
