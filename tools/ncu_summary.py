@@ -105,7 +105,7 @@ def main():
             key = m.group(1) + (m.group(2).lstrip("_") or "fused")
             dram = [d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in ls]
             summary[key] = {
-                **{k: v for k, v in summary.get(key, {}).items() if k.startswith("dram_bytes_per_step") or k == "note"},
+                **{k: v for k, v in summary.get(key, {}).items() if k.startswith("dram_bytes_per_step") or k.endswith("_in_step") or k in ("note", "step_source")},
                 "launches": len(ls),
                 "dram_bytes_per_launch": dram,
                 "duration_s_per_launch": [d.get("gpu__time_duration.sum") for d in ls],
