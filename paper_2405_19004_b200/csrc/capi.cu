@@ -339,10 +339,12 @@ ColorArgs<T> color_args_slab(const pmg_level_s *l, int color, T *x, const T *b, 
 }
 
 template <typename T>
-void smooth_color_impl(pmg_level_s *l, int variant, int color, T *x, const T *b, cudaStream_t s)
+void smooth_color_impl(pmg_level_s *l, int variant, int color, T *x, const T *b, cudaStream_t s,
+                       bool b_ready = false)
 {
   const auto &kt = ktab<T>(l);
   ColorArgs<T> a = color_args<T>(l, color, x, b);
+  a.b_ready = b_ready ? 1 : 0;
   if (a.total == 0)
     return;  // smoother.cpp:57-59: empty colours are skipped
   switch (variant)
@@ -458,13 +460,29 @@ bool sweep_impl(pmg_level_s *l, int variant, T *x, const T *b, cudaStream_t s)
   return kt.sweep(l->patch_mats.data(), sw, variant == PMG_FUSED ? MODE_FUSED : MODE_BOUNDARY, l->sm_count, s);
 }
 
+inline bool b_prefetch_enabled()
+{
+  static const bool v = [] {
+    const char *e = std::getenv("PMG_B_PREFETCH");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 template <typename T>
 void smooth_impl(pmg_level_s *l, int variant, T *x, const T *b, cudaStream_t s)
 {
   if (sweep_impl<T>(l, variant, x, b, s))
     return;
+  // after the first launch of the step b is final (no kernel of the step
+  // writes it): the later colours may prefetch it before their PDL wait
+  bool launched = false;
   for (int color = 0; color < (1 << l->S.dim); ++color)
-    smooth_color_impl<T>(l, variant, color, x, b, s);
+  {
+    smooth_color_impl<T>(l, variant, color, x, b, s,
+                         launched && b_prefetch_enabled() && (variant == PMG_FUSED || variant == PMG_BOUNDARY));
+    launched = launched || color_args<T>(l, color, x, b).total > 0;
+  }
 }
 
 void check_pair(const pmg_level_s *c, const pmg_level_s *f, const char *what)

@@ -166,6 +166,9 @@ struct ColorArgs
   int level_total;  // patches of this colour on the whole unit-cube level: kernel choice
                     // (independent of slab / range restriction, so P slabs dispatch
                     // exactly like one GPU and stay bitwise equal)
+  int b_ready;      // b was final before the previous launch of this stream started (a
+                    // later colour of the same step): kernels may read it before their
+                    // programmatic-dependency wait
 };
 
 template <typename T>

@@ -72,7 +72,7 @@ struct PlaneCfg
 // before (shared memory reuse) and after (the tile's x^I stores are complete).
 template <int K, typename T, int MODE>
 __device__ __forceinline__ void plane_tile(const PatchMatsEO<T, K> &P, const ColorArgs<T> &a, int bx, int j1,
-                                           int j2, unsigned char *smem_raw)
+                                           int j2, unsigned char *smem_raw, bool PRO = false)
 {
   using C = PlaneCfg<K, T>;
   constexpr int NC = C::NC, NI = C::NI, PB = C::PB, NT = C::NT, RX = C::RX;
@@ -92,6 +92,24 @@ __device__ __forceinline__ void plane_tile(const PatchMatsEO<T, K> &P, const Col
   const int G1 = K * (2 * j1 + a.vb[1] - 1) - 1;
   const int64_t G2g = static_cast<int64_t>(K) * (2 * static_cast<int64_t>(j2) + a.vb[2] - 1) - 1;
   const int64_t G2 = G2g - a.zoff;  // local plane of t2 = 0 in x / b
+
+  // ---- b^I of this thread's (p, i0, i1) column, straight into registers (b is
+  //      not written by the smoother: with a.b_ready before the PDL wait) ----
+  const int p24 = tid / NI2;
+  const int rr24 = tid - p24 * NI2;
+  const int i0_24 = rr24 % NI, i1_24 = rr24 / NI;
+  const bool act24 = tid < PB * NI2 && p24 < npv;
+  const int64_t col24 = (G2 + 1) * m2 + static_cast<int64_t>(G1 + 1 + i1_24) * m + (G0 + 2 * K * p24 + 1 + i0_24);
+  T bcol[NI];
+  if (act24)
+  {
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      bcol[i] = __ldg(a.b + col24 + i * m2);
+  }
+
+  if (PRO)
+    pdl_prologue();
 
   // ---- stage the closures of x, zero-filled outside the domain (gather,
   //      patches.cpp:72-79). Thread -> union column (X, t1), then a fixed-stride
@@ -127,20 +145,6 @@ __device__ __forceinline__ void plane_tile(const PatchMatsEO<T, K> &P, const Col
     }
   }
   cp_async_commit();
-
-  // ---- b^I of this thread's (p, i0, i1) column, straight into registers ------
-  const int p24 = tid / NI2;
-  const int rr24 = tid - p24 * NI2;
-  const int i0_24 = rr24 % NI, i1_24 = rr24 / NI;
-  const bool act24 = tid < PB * NI2 && p24 < npv;
-  const int64_t col24 = (G2 + 1) * m2 + static_cast<int64_t>(G1 + 1 + i1_24) * m + (G0 + 2 * K * p24 + 1 + i0_24);
-  T bcol[NI];
-  if (act24)
-  {
-#pragma unroll
-    for (int i = 0; i < NI; ++i)
-      bcol[i] = __ldg(a.b + col24 + i * m2);
-  }
 
   cp_async_wait_all();
   __syncthreads();
@@ -354,9 +358,11 @@ template <int K, typename T, int MODE>
 __global__ void __launch_bounds__(PlaneCfg<K, T>::NT, K == 2 ? PMG_PLANE_MINB : 1)
     vp_smooth_plane_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ ColorArgs<T> a)
 {
-  pdl_prologue();
+  // b_ready: the b^I loads are issued before the dependency wait (inside)
+  if (!a.b_ready)
+    pdl_prologue();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  plane_tile<K, T, MODE>(P, a, blockIdx.x, blockIdx.y, blockIdx.z, smem_raw);
+  plane_tile<K, T, MODE>(P, a, blockIdx.x, blockIdx.y, blockIdx.z, smem_raw, a.b_ready != 0);
 }
 
 // ---------------------------------------------------------------------------

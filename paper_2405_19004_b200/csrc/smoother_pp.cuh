@@ -105,7 +105,10 @@ template <int K, typename T, int MODE>
 __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
     vp_smooth_pp_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ ColorArgs<T> a)
 {
-  pdl_prologue();
+  // b_ready (a later colour of the step): the b^I copies are issued before the
+  // programmatic-dependency wait, the closure copies after it
+  if (!a.b_ready)
+    pdl_prologue();
   using C = PPCfg<K, T>;
   constexpr int NC = C::NC, NI = C::NI, PB = C::PB, UW = C::UW, BW = C::BW;
   constexpr int A_ = 0, B_ = 1, C_ = 2, D_ = 3, E_ = 4, F_ = 5, G_ = 6;
@@ -145,7 +148,39 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
   }
   __syncthreads();
 
-  // ---- stage closure (z-lines, zero fill, patches.cpp:72-79) and b^I -----------
+  // ---- b^I (before the dependency wait when a.b_ready), then the closure
+  //      (z-lines, zero fill, patches.cpp:72-79) ---------------------------------
+  if (tid < PB * NI * NI)
+  {
+    const int p = tid / (NI * NI);
+    const int rr = tid - p * (NI * NI);
+    const int i0 = rr % NI, i1 = rr / NI;
+    const bool ok = org[p][0] > -(1 << 29);
+    if constexpr (PP_INCR_STAGING)
+    {
+      const T *src = ok ? a.b + (static_cast<int64_t>(org[p][2]) + 1 - a.zoff) * m2 +
+                              static_cast<int64_t>(org[p][1] + 1 + i1) * m + (org[p][0] + 1 + i0)
+                        : a.x;
+      const unsigned sdst = smem_addr(Bs + p * BW + rr);
+#pragma unroll
+      for (int t = 0; t < NI; ++t)
+      {
+        cp_async_sa<T>(sdst + static_cast<unsigned>(sizeof(T) * NI * NI * t), src, ok);
+        src += m2;
+      }
+    }
+    else
+    {
+      const T *src = a.b + (static_cast<int64_t>(org[p][2]) + 1 - a.zoff) * m2 +
+                     static_cast<int64_t>(org[p][1] + 1 + i1) * m + (org[p][0] + 1 + i0);
+      T *dst = Bs + p * BW + rr;
+#pragma unroll
+      for (int t = 0; t < NI; ++t)
+        cp_async_elem(dst + NI * NI * t, ok ? src + t * m2 : a.x, ok);
+    }
+  }
+  if (a.b_ready)
+    pdl_prologue();
   if (tid < PB * NC * NC)
   {
     const int p = tid / (NC * NC);
@@ -184,35 +219,6 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
           ok = ok && !(t0 >= 1 && t0 <= NC - 2 && t1 >= 1 && t1 <= NC - 2 && t >= 1 && t <= NC - 2);
         cp_async_elem(dst + NC * NC * t, ok ? src + (zg - a.zoff) * m2 : a.x, ok);
       }
-    }
-  }
-  if (tid < PB * NI * NI)
-  {
-    const int p = tid / (NI * NI);
-    const int rr = tid - p * (NI * NI);
-    const int i0 = rr % NI, i1 = rr / NI;
-    const bool ok = org[p][0] > -(1 << 29);
-    if constexpr (PP_INCR_STAGING)
-    {
-      const T *src = ok ? a.b + (static_cast<int64_t>(org[p][2]) + 1 - a.zoff) * m2 +
-                              static_cast<int64_t>(org[p][1] + 1 + i1) * m + (org[p][0] + 1 + i0)
-                        : a.x;
-      const unsigned sdst = smem_addr(Bs + p * BW + rr);
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-      {
-        cp_async_sa<T>(sdst + static_cast<unsigned>(sizeof(T) * NI * NI * t), src, ok);
-        src += m2;
-      }
-    }
-    else
-    {
-      const T *src = a.b + (static_cast<int64_t>(org[p][2]) + 1 - a.zoff) * m2 +
-                     static_cast<int64_t>(org[p][1] + 1 + i1) * m + (org[p][0] + 1 + i0);
-      T *dst = Bs + p * BW + rr;
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-        cp_async_elem(dst + NI * NI * t, ok ? src + t * m2 : a.x, ok);
     }
   }
   cp_async_commit();
