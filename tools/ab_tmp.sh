@@ -1,5 +1,4 @@
-O=gpurun_out/ab_pers; mkdir -p $O
-PMG_PLANE_PERSIST=1 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "sweep_bitwise or d3k2 or plane" > $O/tests.log 2>&1; tail -2 $O/tests.log
-for r in 1 2; do
-echo "== base" >> $O/qt.log; timeout 300 python tools/quick_time.py 3 2 6 f64 fused 3 2 6 f32 fused 3 2 5 f64 fused >> $O/qt.log 2>&1
-for tpc in 0 -1 2 3; do echo "== persist tpc=$tpc" >> $O/qt.log; PMG_PLANE_PERSIST=1 PMG_PLANE_PERSIST_TPC=$tpc timeout 300 python tools/quick_time.py 3 2 6 f64 fused 3 2 6 f32 fused 3 2 5 f64 fused >> $O/qt.log 2>&1; done; done
+O=gpurun_out/ab_wave; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_env_knobs.py -x -q -m gpu > $O/tests.log 2>&1; tail -3 $O/tests.log
+for r in 1 2; do for cfg in "0 1" "1 1" "1 2" "1 3"; do set -- $cfg; echo "== MIN_N=$1 BLOCK=$2" >> $O/qt.log
+PMG_WAVE_MIN_N=$1 PMG_WAVE_BLOCK=$2 timeout 300 python tools/quick_time.py 3 1 9 f64 fused 3 1 9 f32 fused 3 1 8 f64 fused 3 1 7 f64 fused 3 1 6 f64 fused >> $O/qt.log 2>&1; done; done
