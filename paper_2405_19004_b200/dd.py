@@ -220,6 +220,90 @@ def virtual_smooth(plans, kernels, xs):
                 kernels[r](c, lo, hi)
 
 
+# ---------------------------------------------------------------------------
+# SURVEY.md §8e "alternative to evaluate": ONE exchange per smoothing step
+# instead of one per colour, bought with redundant halo patches. A patch at
+# vertex v reads the dof planes of vertices v-1..v+1 and writes strictly
+# between them. A rank owning vertex planes [a, b] (dof planes k(a-1) ..
+# kb-1, the lowest of which is also written by vertex a-1) must therefore run
+# the last colour on vertices [a-1, b], colour 6 on [a-2, b+1], ..., colour c
+# on [a-1-(7-c), b+(7-c)]: the values each colour reads are then exact —
+# received from their owner at the start of the step or recomputed from exact
+# inputs by the owner's arithmetic — and the owned planes end equal to the
+# single-domain step bitwise. The local slab holds the dof planes of
+# vertices a-9 .. b+8; every non-owned plane of it arrives in one message
+# per neighbour. Cost: the same bytes as the 8 per-colour messages, in one;
+# sum_c (15 - 2c) = 64 extra colour vertex-planes of patches per rank.
+DEEP = 8  # 2^d colours (3D)
+
+
+def deep_halo_plan(plan: SlabPlan) -> SlabPlan:
+    """`plan` with its local slab widened to the dof planes of vertices
+    a - 9 .. b + 8 (clipped to the box); ownership unchanged."""
+    k = plan.k
+    lo = max(0, k * (plan.a - DEEP - 1) - 1)
+    hi = min(plan.mz - 1, k * (plan.b + DEEP) - 1)
+    return SlabPlan(plan.world, plan.rank, plan.k, plan.n, plan.nz, plan.a, plan.b, lo, hi, plan.own_lo,
+                    plan.own_hi)
+
+
+def deep_halo_messages(plans):
+    """Per rank: (sends, recvs) of (peer, first global plane, nplanes) so every
+    rank receives the non-owned planes of its widened slab from their owners."""
+    msgs = [([], []) for _ in plans]
+    for r, p in enumerate(plans):
+        for q, o in enumerate(plans):
+            if q == r:
+                continue
+            g0, g1 = max(p.lo, o.own_lo), min(p.hi, o.own_hi)
+            if g0 <= g1:
+                msgs[q][0].append((r, g0, g1 - g0 + 1))
+                msgs[r][1].append((q, g0, g1 - g0 + 1))
+    return msgs
+
+
+def deep_colour_range(p: SlabPlan, color: int):
+    """Vertex planes colour `color` smooths on this rank in the deep-halo step."""
+    nv = p.nz - 1
+    lo, hi = max(1, p.a - 1 - (DEEP - 1 - color)), min(nv, p.b + (DEEP - 1 - color))
+    return (lo, hi) if lo <= hi and colour_nonempty(p.n, color) else None
+
+
+class DeepHaloSmoother:
+    """One smoothing step with a single halo exchange (see above). plan: a
+    deep_halo_plan; sends / recvs: this rank's entry of deep_halo_messages;
+    kernel(color, vz_lo, vz_hi) and comm as for SlabSmoother."""
+
+    def __init__(self, plan: SlabPlan, sends, recvs, kernel, comm):
+        self.plan, self.kernel, self.comm = plan, kernel, comm
+        self.sends = [(q, g0 - plan.lo, n) for q, g0, n in sends]
+        self.recvs = [(q, g0 - plan.lo, n) for q, g0, n in recvs]
+
+    def smooth(self):
+        if self.sends or self.recvs:
+            self.comm.post(self.sends, self.recvs).wait()
+        for c in range(8):
+            r = deep_colour_range(self.plan, c)
+            if r is not None:
+                self.kernel(c, r[0], r[1])
+
+
+def virtual_deep_smooth(plans, kernels, xs):
+    """deep-halo step for P slabs in one process: owners' planes copied into
+    every widened slab, then each rank's colours."""
+    msgs = deep_halo_messages(plans)
+    for r, p in enumerate(plans):
+        for q, g0, n in msgs[r][1]:
+            o = plans[q]
+            xs[r][(g0 - p.lo) * p.plane_size:(g0 - p.lo + n) * p.plane_size] = \
+                xs[q][(g0 - o.lo) * o.plane_size:(g0 - o.lo + n) * o.plane_size]
+    for r, p in enumerate(plans):
+        for c in range(8):
+            rg = deep_colour_range(p, c)
+            if rg is not None:
+                kernels[r](c, rg[0], rg[1])
+
+
 def scatter_global(plan: SlabPlan, x_global):
     """Local slab (planes lo..hi) of a global flat vector."""
     return x_global[plan.lo * plan.plane_size:(plan.hi + 1) * plan.plane_size]

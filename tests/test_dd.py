@@ -304,3 +304,73 @@ def test_cpp_plan_errors():
     buf = (ctypes.c_int64 * 16)()
     assert _lib.load().pmg_dd_plan(8, 0, 2, 2, 1, buf, 16) < 0  # 3 vertex planes over 8 ranks
     assert _lib.load().pmg_dd_plan(2, 0, 2, 5, 1, buf, 4) < 0   # capacity
+
+
+# ---------------------------------------------------------------------------
+# SURVEY.md §8e alternative: one exchange per step with an 8-vertex-plane
+# halo and redundant halo patches (dd.DeepHaloSmoother) == one domain.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("world,k,level,steps", [(2, 2, 4, 2), (3, 1, 5, 3), (2, 3, 4, 1), (4, 1, 5, 2), (5, 2, 3, 2)])
+def test_virtual_deep_halo_equals_full_smooth(world, k, level, steps):
+    ctx = O.MultigridContext(3, k, level)
+    lc = ctx.levels[-1]
+    rng = np.random.default_rng(5)
+    x0 = rng.uniform(-1, 1, lc.level.total_dofs)
+    b = rng.uniform(-1, 1, lc.level.total_dofs)
+    want = x0.copy()
+    for _ in range(steps):
+        want = O.smooth(lc, want, b)
+    ps = [dd.deep_halo_plan(p) for p in plans_for(world, k, level, 1)]
+    xs = [dd.scatter_global(p, x0).copy() for p in ps]
+    bs = [dd.scatter_global(p, b).copy() for p in ps]
+    for _ in range(steps):
+        dd.virtual_deep_smooth(ps, [oracle_kernel(lc, p, x, bb) for p, x, bb in zip(ps, xs, bs)], xs)
+    got = np.concatenate([dd.owned_part(p, x) for p, x in zip(ps, xs)])
+    np.testing.assert_array_equal(got, want)
+
+
+def _gloo_deep_worker(rank, world, port, k, level, out_path):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lc = O.MultigridContext(3, k, level).levels[-1]
+        plans = [dd.deep_halo_plan(dd.make_plan(world, r, k, level)) for r in range(world)]
+        plan = plans[rank]
+        sends, recvs = dd.deep_halo_messages(plans)[rank]
+        full = dd.make_plan(1, 0, k, level)
+        rng = np.random.default_rng(23)
+        n = full.nplanes * full.plane_size
+        x0, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+        xt = torch.from_numpy(dd.scatter_global(plan, x0).copy())
+        bl = dd.scatter_global(plan, b).copy()
+        sm = dd.DeepHaloSmoother(plan, sends, recvs, oracle_kernel(lc, plan, xt.numpy(), bl),
+                                 dd.TorchDistComm(xt, plan.plane_size))
+        for _ in range(2):
+            sm.smooth()
+        own = torch.from_numpy(dd.owned_part(plan, xt.numpy()).copy())
+        sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([own.numel()]))
+        mx = int(max(s.item() for s in sizes))
+        padded = torch.zeros(mx, dtype=own.dtype)
+        padded[: own.numel()] = own
+        parts = [torch.zeros(mx, dtype=own.dtype) for _ in sizes]
+        dist.all_gather(parts, padded)
+        if rank == 0:
+            got = torch.cat([p[: int(s.item())] for p, s in zip(parts, sizes)]).numpy()
+            want = x0.copy()
+            for _ in range(2):
+                want = O.smooth(lc, want, b)
+            np.save(out_path, np.array([float(np.abs(got - want).max())]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_deep_halo_three_ranks(tmp_path):
+    """The single-exchange step over torch.distributed (gloo, world 3)."""
+    out = str(tmp_path / "err.npy")
+    mp.spawn(_gloo_deep_worker, args=(3, _free_port(), 2, 4, out), nprocs=3, join=True)
+    assert np.load(out)[0] == 0.0
