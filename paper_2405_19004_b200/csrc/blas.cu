@@ -6,6 +6,8 @@
 // reproducible run to run (no atomics), accumulated in f64.
 #include "blas.cuh"
 
+#include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace pmgb
@@ -244,6 +246,113 @@ __global__ void __launch_bounds__(256) coarse_gemv_kernel(const T *__restrict__ 
     x[row] = sum;
 }
 
+// Same product, the operator streamed by TMA (1D cp.async.bulk, completion on
+// an mbarrier transaction count): each warp owns one shared-memory row
+// buffer, its lane 0 issues the bulk copy of the warp's next row as soon as
+// the lanes have consumed the current one, so every SM keeps NW rows
+// (~NW x 27 KB at 3375 unknowns) in flight with no register staging; the
+// first rows are requested before the programmatic-dependency wait. The dot
+// product and its reduction are coarse_gemv_kernel's per-lane order.
+__device__ __forceinline__ unsigned gv_smem(const void *p)
+{
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 1) coarse_gemv_bulk_kernel(const T *__restrict__ M, const T *__restrict__ b,
+                                                                 T *__restrict__ x, int n, int ld)
+{
+  using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+  constexpr int W = 16 / sizeof(T), U = 4;
+  extern __shared__ __align__(128) unsigned char gb_smem[];
+  __shared__ __align__(8) unsigned long long full[8];
+  const int nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned row_bytes = static_cast<unsigned>(ld * sizeof(T));
+  T *bs = reinterpret_cast<T *>(gb_smem);
+  T *rowbuf = bs + ld + ((16 / sizeof(T)) - (ld % (16 / sizeof(T)))) % (16 / sizeof(T)) + 0;
+  T *mine = rowbuf + static_cast<size_t>(warp) * ld;
+  const unsigned bar = gv_smem(&full[warp]);
+  const int G = gridDim.x;
+  int row = blockIdx.x + warp * G;
+  if (lane == 0)
+  {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (row < n)
+    {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       gv_smem(mine)),
+                   "l"(M + static_cast<int64_t>(row) * ld), "r"(row_bytes), "r"(bar)
+                   : "memory");
+    }
+  }
+  pdl_prologue();
+  for (int j = threadIdx.x; j < ld; j += blockDim.x)
+    bs[j] = j < n ? b[j] : T(0);
+  __syncthreads();
+  const V *bv = reinterpret_cast<const V *>(bs);
+  const V *mv = reinterpret_cast<const V *>(mine);
+  const int nv = ld / W;
+  unsigned phase = 0;
+  for (; row < n; row += nw * G)
+  {
+    // wait for this warp's row
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(bar), "r"(phase)
+                   : "memory");
+    phase ^= 1u;
+    T acc[U] = {T(0), T(0), T(0), T(0)};
+    int c = lane;
+    for (; c + 32 * (U - 1) < nv; c += 32 * U)
+    {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+      {
+        const V m4 = mv[c + 32 * u], b4 = bv[c + 32 * u];
+        const T *mm = reinterpret_cast<const T *>(&m4);
+        const T *bq = reinterpret_cast<const T *>(&b4);
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          acc[u] = fma(mm[w], bq[w], acc[u]);
+      }
+    }
+    for (; c < nv; c += 32)
+    {
+      const V m4 = mv[c], b4 = bv[c];
+      const T *mm = reinterpret_cast<const T *>(&m4);
+      const T *bq = reinterpret_cast<const T *>(&b4);
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        acc[0] = fma(mm[w], bq[w], acc[0]);
+    }
+    T sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const int nrow = row + nw * G;
+    __syncwarp();  // every lane's reads of the buffer are done (their values fed the sum)
+    if (lane == 0)
+    {
+      x[row] = sum;
+      if (nrow < n)
+      {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(gv_smem(mine)),
+            "l"(M + static_cast<int64_t>(nrow) * ld), "r"(row_bytes), "r"(bar)
+            : "memory");
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <typename T>
 __global__ void unit_kernel(T *x, int n, int j)
 {
@@ -299,6 +408,37 @@ template void launch_store_column<float>(float *, const float *, int, int, int *
 template <typename T>
 void launch_coarse_gemv(const T *M, const T *b, T *x, int n, int ld, cudaStream_t s)
 {
+  // TMA-streamed variant: measured faster for f32 (11.7 vs 13.0 us at 3375
+  // unknowns), slower for f64 (26.9 vs 23.8 us; profiles/r02/ab/gemv/bulk.txt);
+  // PMG_GEMV_BULK=0 / 1 forces either
+  static const int bulk_env = [] {
+    const char *e = std::getenv("PMG_GEMV_BULK");
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  const bool bulk = bulk_env < 0 ? sizeof(T) == 4 : bulk_env == 1;
+  if (bulk)
+  {
+    // b + one row buffer per warp, up to 8 warps within 220 KB
+    const size_t rowb = static_cast<size_t>(ld) * sizeof(T);
+    const size_t budget = 220 * 1024;
+    const int nw = static_cast<int>(std::min<size_t>(8, (budget - rowb - 16) / rowb));
+    if (nw >= 2)
+    {
+      const size_t smem = rowb + 16 + static_cast<size_t>(nw) * rowb;
+      static unsigned bmask = 0;
+      if (first_on_device(bmask))
+        check_cuda(cudaFuncSetAttribute(coarse_gemv_bulk_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(budget + 1024)),
+                   "cudaFuncSetAttribute(coarse_gemv_bulk)");
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      const int grid = std::max(1, std::min(nsm, (n + nw - 1) / nw));
+      pdl_launch(coarse_gemv_bulk_kernel<T>, dim3(grid), dim3(32 * nw), smem, s, M, b, x, n, ld);
+      check_launch("coarse_gemv_bulk_kernel");
+      return;
+    }
+  }
   const size_t smem = static_cast<size_t>(ld) * sizeof(T);
   static unsigned attr_mask = 0;
   if (first_on_device(attr_mask))
