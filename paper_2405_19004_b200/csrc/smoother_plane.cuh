@@ -62,6 +62,9 @@ struct PlaneCfg
   static constexpr size_t SMEM = static_cast<size_t>(PB) * (UW + WW) * sizeof(T);
 };
 
+#ifndef PMG_PLANE_ZMASK
+#define PMG_PLANE_ZMASK 1
+#endif
 #ifndef PMG_PLANE_MINB
 #define PMG_PLANE_MINB 5
 #endif
@@ -116,6 +119,13 @@ __device__ __forceinline__ void plane_tile(const PatchMatsEO<T, K> &P, const Col
   //      walk over the NC planes t2; lanes run along contiguous x. Column X
   //      belongs to patch X / 2K (t0 = X mod 2K) and, on a shared vertex column,
   //      also to patch X / 2K - 1 (t0 = 2K). ------------------------------------
+#if PMG_PLANE_ZMASK
+  // z validity of the NC closure planes: CTA-uniform, one bit per plane
+  unsigned zmask = 0;
+#pragma unroll
+  for (int t2 = 0; t2 < NC; ++t2)
+    zmask |= (static_cast<uint64_t>(G2g + t2) < static_cast<uint64_t>(a.mz) ? 1u : 0u) << t2;
+#endif
 #pragma unroll 1
   for (int line = tid; line < NC * RX; line += NT)
   {
@@ -134,7 +144,11 @@ __device__ __forceinline__ void plane_tile(const PatchMatsEO<T, K> &P, const Col
 #pragma unroll
     for (int t2 = 0; t2 < NC; ++t2)
     {
+#if PMG_PLANE_ZMASK
+      const bool ok = okxy && ((zmask >> t2) & 1u);
+#else
       const bool ok = okxy && static_cast<uint64_t>(G2g + t2) < static_cast<uint64_t>(a.mz);
+#endif
       bool ok1 = ok;
       if constexpr (MODE == MODE_BOUNDARY)  // never reads x^I (smoother.cpp:128-148)
         ok1 = ok && !(t0 >= 1 && t0 <= NC - 2 && t1 >= 1 && t1 <= NC - 2 && t2 >= 1 && t2 <= NC - 2);
