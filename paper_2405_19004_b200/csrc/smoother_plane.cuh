@@ -62,6 +62,9 @@ struct PlaneCfg
   static constexpr size_t SMEM = static_cast<size_t>(PB) * (UW + WW) * sizeof(T);
 };
 
+#ifndef PMG_PLANE_SADDR
+#define PMG_PLANE_SADDR 1
+#endif
 #ifndef PMG_PLANE_ZMASK
 #define PMG_PLANE_ZMASK 1
 #endif
@@ -140,6 +143,10 @@ __device__ __forceinline__ void plane_tile(const PatchMatsEO<T, K> &P, const Col
     const bool dup = t0 == 0 && p > 0;
     T *dst = U + p * UW + t1 * SU1 + t0;
     T *dst2 = U + (p - 1) * UW + t1 * SU1 + 2 * K;
+#if PMG_PLANE_SADDR
+    // shared-window addresses once per line; per plane a compile-time stride
+    const unsigned sd = smem_addr(dst), sd2 = smem_addr(dst2);
+#endif
     const T *src = a.x + G2 * m2 + static_cast<int64_t>(gy) * m + gx;
 #pragma unroll
     for (int t2 = 0; t2 < NC; ++t2)
@@ -153,9 +160,15 @@ __device__ __forceinline__ void plane_tile(const PatchMatsEO<T, K> &P, const Col
       if constexpr (MODE == MODE_BOUNDARY)  // never reads x^I (smoother.cpp:128-148)
         ok1 = ok && !(t0 >= 1 && t0 <= NC - 2 && t1 >= 1 && t1 <= NC - 2 && t2 >= 1 && t2 <= NC - 2);
       const T *sp = ok ? src + t2 * m2 : a.x;
+#if PMG_PLANE_SADDR
+      cp_async_sa<T>(sd + static_cast<unsigned>(sizeof(T) * SU2 * t2), sp, ok1);
+      if (dup)
+        cp_async_sa<T>(sd2 + static_cast<unsigned>(sizeof(T) * SU2 * t2), sp, ok);
+#else
       cp_async_elem(dst + t2 * SU2, sp, ok1);
       if (dup)
         cp_async_elem(dst2 + t2 * SU2, sp, ok);
+#endif
     }
   }
   cp_async_commit();
