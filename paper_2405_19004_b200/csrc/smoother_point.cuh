@@ -27,16 +27,19 @@ struct PointStencil
   T coef;
 };
 
-template <int D, typename T, int MODE>
-__global__ void __launch_bounds__(128) vp_point_kernel(const __grid_constant__ PointStencil<T> st,
-                                                       const __grid_constant__ ColorArgs<T> a)
+// patches per thread (consecutive rows j1, independent stencils in flight):
+// 2 in f32 (3D Q1 L9 83 -> 92 GDoF/s, 2D Q1 L14 124 -> 166), 1 in f64 (2
+// costs 4-12% there: profiles/r02/ab/point_ppt.txt)
+template <typename T>
+constexpr int point_ppt()
 {
-  pdl_prologue();
-  const int j0 = blockIdx.x * 32 + threadIdx.x;
-  const int j1 = blockIdx.y * 4 + threadIdx.y;
-  const int j2 = D == 3 ? static_cast<int>(blockIdx.z) : 0;
-  if (j0 >= a.np[0] || j1 >= a.np[1])
-    return;
+  return sizeof(T) == 4 ? 2 : 1;
+}
+
+// patch (j0, j1, j2) of the colour a
+template <int D, typename T, int MODE>
+__device__ __forceinline__ void point_patch(const PointStencil<T> &st, const ColorArgs<T> &a, int j0, int j1, int j2)
+{
   const int64_t m = a.m;
   // centre node c_a = v_a - 1, v_a = 2 j_a + vb_a
   const int c0 = 2 * j0 + a.vb[0] - 1;
@@ -82,12 +85,30 @@ __global__ void __launch_bounds__(128) vp_point_kernel(const __grid_constant__ P
 }
 
 template <int D, typename T, int MODE>
+__global__ void __launch_bounds__(128) vp_point_kernel(const __grid_constant__ PointStencil<T> st,
+                                                       const __grid_constant__ ColorArgs<T> a)
+{
+  pdl_prologue();
+  const int j0 = blockIdx.x * 32 + threadIdx.x;
+  const int j2 = D == 3 ? static_cast<int>(blockIdx.z) : 0;
+  if (j0 >= a.np[0])
+    return;
+#pragma unroll
+  for (int q = 0; q < point_ppt<T>(); ++q)
+  {
+    const int j1 = (blockIdx.y * 4 + threadIdx.y) * point_ppt<T>() + q;
+    if (j1 < a.np[1])
+      point_patch<D, T, MODE>(st, a, j0, j1, j2);
+  }
+}
+
+template <int D, typename T, int MODE>
 void launch_vp_point(const PointStencil<T> &st, const ColorArgs<T> &a, cudaStream_t s)
 {
   if (a.total == 0)
     return;
   dim3 block(32, 4, 1);
-  dim3 grid((a.np[0] + 31) / 32, (a.np[1] + 3) / 4, D == 3 ? a.np[2] : 1);
+  dim3 grid((a.np[0] + 31) / 32, (a.np[1] + 4 * point_ppt<T>() - 1) / (4 * point_ppt<T>()), D == 3 ? a.np[2] : 1);
   pdl_launch(vp_point_kernel<D, T, MODE>, grid, block, 0, s, st, a);
   check_launch("vp_point_kernel");
 }
