@@ -111,7 +111,8 @@ __device__ __forceinline__ void plane_tile(const PatchMatsEO<T, K> &P, const Col
   {
 #pragma unroll
     for (int i = 0; i < NI; ++i)
-      bcol[i] = __ldg(a.b + col24 + i * m2);
+      bcol[i] = PRO ? __ldcg(a.b + col24 + i * m2)  // before the PDL wait: L2 only, no L1 line
+                    : __ldg(a.b + col24 + i * m2);  // that predates the wait can be hit
   }
 
   if (PRO)

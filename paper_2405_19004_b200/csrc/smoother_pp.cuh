@@ -105,10 +105,11 @@ template <int K, typename T, int MODE>
 __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
     vp_smooth_pp_kernel(const __grid_constant__ PatchMatsEO<T, K> P, const __grid_constant__ ColorArgs<T> a)
 {
-  // b_ready (a later colour of the step): the b^I copies are issued before the
-  // programmatic-dependency wait, the closure copies after it
-  if (!a.b_ready)
-    pdl_prologue();
+  // (the plane kernel reads b before the programmatic-dependency wait for
+  // the later colours of a step; this kernel stages b with cp.async, which
+  // goes through L1, so it waits first: a pre-wait read could hit an L1 line
+  // older than the wait's visibility guarantee)
+  pdl_prologue();
   using C = PPCfg<K, T>;
   constexpr int NC = C::NC, NI = C::NI, PB = C::PB, UW = C::UW, BW = C::BW;
   constexpr int A_ = 0, B_ = 1, C_ = 2, D_ = 3, E_ = 4, F_ = 5, G_ = 6;
@@ -148,8 +149,7 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
   }
   __syncthreads();
 
-  // ---- b^I (before the dependency wait when a.b_ready), then the closure
-  //      (z-lines, zero fill, patches.cpp:72-79) ---------------------------------
+  // ---- b^I, then the closure (z-lines, zero fill, patches.cpp:72-79) --------
   if (tid < PB * NI * NI)
   {
     const int p = tid / (NI * NI);
@@ -179,8 +179,6 @@ __global__ void __launch_bounds__(sm_nt<3, K, T>(), sm_minb<3, K, T>())
         cp_async_elem(dst + NI * NI * t, ok ? src + t * m2 : a.x, ok);
     }
   }
-  if (a.b_ready)
-    pdl_prologue();
   if (tid < PB * NC * NC)
   {
     const int p = tid / (NC * NC);
