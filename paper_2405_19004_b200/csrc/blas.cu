@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256) coarse_gemv_kernel(const T *__restrict__ 
   {
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      cur[u] = __ldcs(mr + lane + 32 * u);
+      cur[u] = __ldcg(mr + lane + 32 * u);  // before the PDL wait: L2 only
   }
   pdl_prologue();
   T *bs = reinterpret_cast<T *>(gemv_smem);  // [ld], zero padded
